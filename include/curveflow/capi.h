@@ -1,0 +1,144 @@
+/*
+ * include/curveflow/capi.h -- C-ABI of the B200-native WMC path
+ * (libcurveflow_b200.so, built from paper_1903_07189_b200/csrc/).
+ *
+ * The reference (arXiv 1903.07189, /root/reference) declares this path only
+ * in its spec; its proj/include holds just the CPU executor
+ * curveflow::parallel (proj/include/curveflow/parallel.hpp:7-49).  The entry
+ * points below are the drop-in for the two SPEC operations on the path:
+ *
+ *   wmc_half_laplace(img: Image2D) -> Image2D
+ *   mc_flow(img: Image2D, cfg: FlowConfig) -> Image2D
+ *                                  (cfg.scheme == half_laplace only)
+ *
+ * and the pieces of the spec they rely on: per-channel planes
+ * (SPEC.md:62-69), 8-bit widening on load, non-finite abort
+ * naming the iteration, bit-identical output for any
+ * parallel decomposition (parallel.hpp:23-25).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross the ABI.
+ *  - Image pointers passed to cf_wmc_* are DEVICE pointers owned by the
+ *    caller, valid until the work enqueued on `stream` (a cudaStream_t passed
+ *    as void*, NULL = legacy default stream) completes.  Calls are
+ *    stream-ordered and asynchronous unless stated otherwise.
+ *  - Images are planar fp32, row-major: element (plane p, row y, col x) is
+ *    base[p*plane_stride + y*pitch + x], pitch >= w, all in ELEMENTS.
+ *  - Returns CF_OK (0) or a status below; no exceptions cross the ABI.
+ *    CF_ECUDA keeps the CUDA error in thread-local state (cf_last_cuda_error).
+ *  - Re-entrant: concurrent calls on different streams are safe.
+ *  - Results are bit-identical for every launch configuration, temporal
+ *    depth and band decomposition, and equal to the canonical fp32
+ *    evaluation documented in DESIGN.md §3 (oracle/wmc_oracle.c).
+ */
+#ifndef CURVEFLOW_CAPI_H
+#define CURVEFLOW_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CF_API __attribute__((visibility("default")))
+#else
+#define CF_API
+#endif
+
+enum cf_status {
+    CF_OK = 0,
+    CF_EINVAL = 1,      /* bad shape / pitch / planes / iters / dt / workspace */
+    CF_ECUDA = 2,       /* CUDA runtime error, see cf_last_cuda_error()         */
+    CF_ENONFINITE = 3,  /* mc_flow produced a non-finite value    */
+    CF_ENODEV = 4       /* no usable sm_100 device                              */
+};
+
+/* Library version string, e.g. "curveflow-b200 0.1.0 (sm_100a)". */
+CF_API const char* cf_version(void);
+/* Human-readable text for a cf_status value. */
+CF_API const char* cf_status_string(int status);
+/* Last CUDA error code recorded on this thread by a call returning CF_ECUDA. */
+CF_API int cf_last_cuda_error(void);
+
+/* ---------------------------------------------------------------------- */
+/* wmc_half_laplace (Eqs. 27-28)                  */
+/* out[p][y][x] = d_m, m = argmin_i |(h_i * in)(y,x)|, ties -> smallest i,  */
+/* clamp-to-edge borders.  out must not alias in.      */
+/* ---------------------------------------------------------------------- */
+CF_API int cf_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
+                          int32_t planes, int64_t plane_stride, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* mc_flow, scheme = half_laplace (Eq. 26)        */
+/* img <- U^iters with U^{t+1} = U^t + dt * wmc_half_laplace(U^t), Jacobi.  */
+/* In-place API; ping-pongs through `workspace`                            */
+/* (>= cf_wmc_filter_workspace_bytes bytes of device memory).              */
+/* dt in (0, 1], iters >= 0 (0 = identity).     */
+/* If first_bad_iter != NULL the call synchronises `stream` and returns    */
+/* CF_ENONFINITE with *first_bad_iter = the first iteration t (1-based)    */
+/* whose iterate holds a NaN/Inf, else sets it to 0.   */
+/* If first_bad_iter == NULL the call is fully asynchronous and the check  */
+/* result can be read later with cf_wmc_filter_query_nonfinite().          */
+/* ---------------------------------------------------------------------- */
+CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                                            int64_t plane_stride);
+CF_API int cf_wmc_filter_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                             int64_t plane_stride, int32_t iters, float dt, void* workspace,
+                             size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
+/* Synchronises `stream`; returns CF_OK / CF_ENONFINITE for the last filter
+ * call that used `workspace`, writing the iteration to *first_bad_iter.   */
+CF_API int cf_wmc_filter_query_nonfinite(const void* workspace, int32_t* first_bad_iter,
+                                         void* stream);
+
+/* 8-bit batch variant (BASELINE cfg 5): in is u8, widened on device as    */
+/* (float)q / 255.0f (IEEE division) inside the first sweep;   */
+/* out receives U^iters in fp32.  in_pitch / in_plane_stride in BYTES.     */
+/* iters == 0 writes the widened image.                                    */
+CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
+                                float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                                int64_t plane_stride, int32_t iters, float dt, void* workspace,
+                                size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Row-band primitive for sharded filtering (BASELINE cfg 4).               */
+/* Runs `sweeps` (1 <= sweeps <= cf_wmc_max_sweeps_per_launch()) Jacobi     */
+/* sweeps of the flow in ONE launch, producing global rows [y0, y1) of the  */
+/* iterate U^{iter_base+sweeps} into dst, from U^{iter_base} in src.        */
+/* src holds global rows [src_row0, src_row0 + src_rows) at                */
+/* src + (y - src_row0) * pitch and must cover                             */
+/* [max(0, y0 - sweeps), min(h, y1 + sweeps)); dst row y is written at      */
+/* dst + (y - dst_row0) * pitch.  h is the GLOBAL height (clamp-to-edge    */
+/* applies only at rows 0 and h-1).  d_flag (device int32, nullable) is    */
+/* atomically min-ed with the first iteration producing a non-finite value.*/
+/* ---------------------------------------------------------------------- */
+CF_API int32_t cf_wmc_max_sweeps_per_launch(void);
+CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,
+                                  float* dst, int32_t dst_row0, int32_t w, int32_t h,
+                                  int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,
+                                  float dt, int32_t iter_base, int32_t* d_flag, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Seeded synthetic image generator (BASELINE.json configs). */
+/* HOST memory, deterministic for a given (seed, params) on any thread     */
+/* count: linear ramp background, n_rects axis-aligned rectangles then     */
+/* n_discs discs of U(0,1) intensity, + N(0, sigma^2) noise, clamp [0,1].  */
+/* f32: value rounded to nearest fp32.  u8: lrint(255 * value).            */
+/* threads <= 0 -> hardware concurrency.                                   */
+/* ---------------------------------------------------------------------- */
+CF_API int cf_synth_f32(float* out, int32_t w, int32_t h, int64_t pitch, uint64_t seed,
+                        int32_t n_rects, int32_t n_discs, double sigma, int32_t threads);
+CF_API int cf_synth_u8(uint8_t* out, int32_t w, int32_t h, int64_t pitch, uint64_t seed,
+                       int32_t n_rects, int32_t n_discs, double sigma, int32_t threads);
+
+/* ---------------------------------------------------------------------- */
+/* Kernel bank: h_i weights times 12 as exact integers,  */
+/* out72[i*9 + r*3 + c], i = 0..7 for h1..h8, r/c = dy+1 / dx+1.          */
+/* ---------------------------------------------------------------------- */
+CF_API void cf_kernel_bank_x12(int32_t* out72);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CURVEFLOW_CAPI_H */

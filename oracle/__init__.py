@@ -1,0 +1,153 @@
+"""CPU oracle for the WMC path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs import this package, always as the checker or the timed
+reference CPU path; the product (paper_1903_07189_b200/) never does.
+
+Wraps oracle/liboracle.so (wmc_oracle.c: fp64 SPEC-faithful + fp32 canonical
+restatement) and, when built, oracle/_ref/libcf_ref.so (the fp64 restatement
+run on the reference's own curveflow::parallel executor).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_REF = os.path.join(_HERE, "_ref", "libcf_ref.so")
+_lib = None
+_ref = None
+
+_i32, _i64, _f32, _f64, _vp = C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p
+_pi32 = C.POINTER(C.c_int32)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise RuntimeError(f"{_LIB} missing: run `make -C oracle` (or __graft_entry__.build())")
+        L = C.CDLL(_LIB)
+        L.or_wmc_map_f64.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp]
+        L.or_wmc_map_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32]
+        L.or_flow_f32.argtypes = [_vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32, _i32, _pi32]
+        L.or_flow_f64.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32, _pi32]
+        L.or_u8_to_f32.argtypes = [_vp, _vp, _i64]
+        L.or_wmc_naive_f64.argtypes = [_vp, _vp, _i32, _i32]
+        L.or_kernel_bank_numerators.argtypes = [_pi32]
+        for f in ("or_wmc_map_f64", "or_wmc_map_f32", "or_flow_f32", "or_flow_f64"):
+            getattr(L, f).restype = C.c_int
+        L.or_u8_to_f32.restype = None
+        L.or_wmc_naive_f64.restype = None
+        _lib = L
+    return _lib
+
+
+def ref_lib():
+    """The reference-executor build, or None if it was never built."""
+    global _ref
+    if _ref is None and os.path.exists(_REF):
+        L = C.CDLL(_REF)
+        L.ref_wmc_map_f64.argtypes = [_vp, _vp, _i32, _i32, _i32]
+        L.ref_flow_f64.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32, _pi32]
+        L.ref_wmc_map_f64.restype = C.c_int
+        L.ref_flow_f64.restype = C.c_int
+        _ref = L
+    return _ref
+
+
+def _threads(t):
+    return os.cpu_count() or 1 if t is None else t
+
+
+def wmc_map_f64(img, threads=None, return_argmin=False):
+    a = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = a.shape
+    out = np.empty_like(a)
+    am = np.empty((h, w), dtype=np.int8) if return_argmin else None
+    rc = lib().or_wmc_map_f64(a.ctypes.data, out.ctypes.data, w, h, _threads(threads),
+                              am.ctypes.data if am is not None else None)
+    assert rc == 0
+    return (out, am) if return_argmin else out
+
+
+def wmc_naive_f64(img):
+    a = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = a.shape
+    out = np.empty_like(a)
+    lib().or_wmc_naive_f64(a.ctypes.data, out.ctypes.data, w, h)
+    return out
+
+
+def wmc_map_f32(img, threads=None):
+    """fp32 canonical map; img (H, W) or (P, H, W)."""
+    a = np.ascontiguousarray(img, dtype=np.float32)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    out = np.empty_like(a3)
+    rc = lib().or_wmc_map_f32(a3.ctypes.data, out.ctypes.data, w, h, w, P, h * w,
+                              _threads(threads))
+    assert rc == 0
+    return out[0] if a.ndim == 2 else out
+
+
+def flow_f32(img, iters, dt=1.0, threads=None):
+    """fp32 canonical mc_flow; returns (U^iters, first_bad_iter or 0)."""
+    a = np.array(img, dtype=np.float32, order="C", copy=True)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    bad = C.c_int32(0)
+    rc = lib().or_flow_f32(a3.ctypes.data, w, h, w, P, h * w, int(iters), float(dt),
+                           _threads(threads), C.byref(bad))
+    assert rc in (0, 3), rc
+    return (a3[0] if a.ndim == 2 else a3), bad.value
+
+
+def flow_f64(img, iters, dt=1.0, threads=None):
+    a = np.array(img, dtype=np.float64, order="C", copy=True)
+    h, w = a.shape
+    bad = C.c_int32(0)
+    rc = lib().or_flow_f64(a.ctypes.data, w, h, int(iters), float(dt), _threads(threads),
+                           C.byref(bad))
+    assert rc in (0, 3), rc
+    return a, bad.value
+
+
+def ref_flow_f64(img, iters, dt=1.0, threads=None):
+    L = ref_lib()
+    if L is None:
+        raise RuntimeError("oracle/_ref/libcf_ref.so not built")
+    a = np.array(img, dtype=np.float64, order="C", copy=True)
+    h, w = a.shape
+    bad = C.c_int32(0)
+    rc = L.ref_flow_f64(a.ctypes.data, w, h, int(iters), float(dt), _threads(threads),
+                        C.byref(bad))
+    assert rc in (0, 3), rc
+    return a, bad.value
+
+
+def ref_wmc_map_f64(img, threads=None):
+    L = ref_lib()
+    if L is None:
+        raise RuntimeError("oracle/_ref/libcf_ref.so not built")
+    a = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = a.shape
+    out = np.empty_like(a)
+    assert L.ref_wmc_map_f64(a.ctypes.data, out.ctypes.data, w, h, _threads(threads)) == 0
+    return out
+
+
+def u8_to_f32(q):
+    q = np.ascontiguousarray(q, dtype=np.uint8)
+    out = np.empty(q.shape, dtype=np.float32)
+    lib().or_u8_to_f32(q.ctypes.data, out.ctypes.data, q.size)
+    return out
+
+
+def kernel_bank_x12():
+    buf = (C.c_int32 * 72)()
+    lib().or_kernel_bank_numerators(buf)
+    return np.array(list(buf), dtype=np.int32).reshape(8, 3, 3)

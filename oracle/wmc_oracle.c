@@ -1,0 +1,287 @@
+/*
+ * oracle/wmc_oracle.c -- CPU restatement of the reference's WMC path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product (paper_1903_07189_b200/,
+ * include/) includes, links or calls this file.  It is used by tests/,
+ * __graft_entry__.smoke() and the cpu_baseline / --impl reference legs of
+ * bench.py, always as the checker / the timed reference CPU path, never as
+ * the thing shipped.
+ *
+ * The reference (/root/reference) ships no implementation of this path, only
+ * a normative spec; every function below cites the SPEC / PAPER lines it
+ * restates.  Two instantiations:
+ *
+ *  1. fp64 "SPEC-faithful" (or_*_f64): per pixel, the eight stencils h1..h8
+ *     (exact rationals lowered to double once) are correlated
+ *     with the clamp-to-edge image in row-major tap order (SPEC.md:53-57,
+ *     :77-78), and the response with the smallest |d_i| is returned, ties to
+ *     the smallest index.  This is
+ *     the "reference CPU path" that bench.py times.
+ *
+ *  2. fp32 "canonical" (or_*_f32): the integer-weight form of SURVEY.md
+ *     Appendix A with every rounding pinned (which sums are formed, their
+ *     operand order, where an FMA is used).  The CUDA kernels evaluate exactly
+ *     this sequence, so GPU-vs-oracle parity is bit-exact.  It is itself
+ *     checked against (1) within 1e-5 (tests/test_oracle.py).
+ *
+ * Flow: U^{t+1} = U^t + dt*H^w(U^t),
+ * synchronous (Jacobi), non-finite check after every iteration naming the
+ * iteration.
+ *
+ * Row parallelism follows curveflow::parallel::for_rows
+ * (proj/include/curveflow/parallel.hpp:26-47): contiguous ceil-div row
+ * blocks, one per worker, caller runs block 0, serial if height < 16 or one
+ * worker.  Output is bit-identical for any thread count (parallel.hpp:23-25).
+ *
+ * Build: oracle/Makefile, gcc -O2 -ffp-contract=off (no -ffast-math), SSE
+ * arithmetic (x86-64 default), so every + and * rounds once to the declared
+ * type and fmaf()/fma() are the only fused operations.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+#define OR_EXPORT __attribute__((visibility("default")))
+
+#include "wmc_px.h"
+
+OR_EXPORT void or_kernel_bank_numerators(int32_t* out72) { kernel_bank_numerators(out72); }
+
+/* ------------------------------------------------------------------------ */
+/* for_rows restatement (parallel.hpp:26-47)                                 */
+/* ------------------------------------------------------------------------ */
+typedef void (*row_fn)(void* ctx, int y);
+
+typedef struct {
+    row_fn fn;
+    void* ctx;
+    int y0, y1;
+} row_block;
+
+static void* run_block(void* arg) {
+    row_block* b = (row_block*)arg;
+    for (int y = b->y0; y < b->y1; ++y) b->fn(b->ctx, y);
+    return NULL;
+}
+
+static void for_rows(int height, int threads, row_fn fn, void* ctx) {
+    int workers = threads < 1 ? 1 : threads;          /* parallel.hpp:28 */
+    if (workers > height) workers = height;            /* :29 */
+    if (workers <= 1 || height < 16) {                 /* :30-33 */
+        for (int y = 0; y < height; ++y) fn(ctx, y);
+        return;
+    }
+    int chunk = (height + workers - 1) / workers;      /* :36 */
+    pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)workers);
+    row_block* blk = (row_block*)malloc(sizeof(row_block) * (size_t)workers);
+    int started = 0;
+    for (int w = 1; w < workers; ++w) {                /* :37-44 */
+        int y0 = w * chunk;
+        int y1 = y0 + chunk < height ? y0 + chunk : height;
+        if (y0 >= y1) break;
+        blk[w].fn = fn; blk[w].ctx = ctx; blk[w].y0 = y0; blk[w].y1 = y1;
+        pthread_create(&tid[w], NULL, run_block, &blk[w]);
+        started = w;
+    }
+    blk[0].fn = fn; blk[0].ctx = ctx; blk[0].y0 = 0;   /* :45 caller runs block 0 */
+    blk[0].y1 = chunk < height ? chunk : height;
+    run_block(&blk[0]);
+    for (int w = 1; w <= started; ++w) pthread_join(tid[w], NULL);  /* :46 */
+    free(tid);
+    free(blk);
+}
+
+
+/* ------------------------------------------------------------------------ */
+/* fp64 SPEC-faithful WMC map                                                */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const double* in;
+    double* out;
+    int w, h;
+    int64_t pitch;
+    int8_t* argmin; /* optional: index 0..7 of the selected kernel */
+} map64_ctx;
+
+static void map64_row(void* vctx, int y) {
+    map64_ctx* c = (map64_ctx*)vctx;
+    for (int x = 0; x < c->w; ++x) {
+        int m;
+        c->out[(int64_t)y * c->pitch + x] = wmc_px_f64(c->in, c->w, c->h, c->pitch, y, x, &m);
+        if (c->argmin) c->argmin[(int64_t)y * c->w + x] = (int8_t)m;
+    }
+}
+
+/* wmc_half_laplace, fp64.  Dense row-major, pitch = w. */
+OR_EXPORT int or_wmc_map_f64(const double* in, double* out, int32_t w, int32_t h,
+                             int32_t threads, int8_t* argmin /* nullable, w*h */) {
+    if (w <= 0 || h <= 0) return 1;
+    pthread_once(&hw_once, init_hw64);
+    map64_ctx c = {in, out, w, h, w, argmin};
+    for_rows(h, threads, map64_row, &c);
+    return 0;
+}
+
+static inline float wmc_at_f32(const float* in, int w, int h, int64_t pitch, int y, int x) {
+    const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
+    const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
+    const float* R0 = in + (int64_t)ym * pitch;
+    const float* R1 = in + (int64_t)y * pitch;
+    const float* R2 = in + (int64_t)yp * pitch;
+    return wmc_px_f32(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x], R2[xp]);
+}
+
+typedef struct {
+    const float* in;
+    float* out;
+    int w, h;
+    int64_t pitch;
+    int flow;  /* 0: out = H^w ; 1: out = fmaf(dt, H^w, u) */
+    float dt;
+    volatile int* bad; /* per-row non-finite marker (flow only) */
+} map32_ctx;
+
+static void map32_row(void* vctx, int y) {
+    map32_ctx* c = (map32_ctx*)vctx;
+    const float* in = c->in;
+    float* o = c->out + (int64_t)y * c->pitch;
+    int bad = 0;
+    for (int x = 0; x < c->w; ++x) {
+        float hw = wmc_at_f32(in, c->w, c->h, c->pitch, y, x);
+        if (c->flow) {
+            float v = fmaf(c->dt, hw, in[(int64_t)y * c->pitch + x]);
+            if (!isfinite(v)) bad = 1;
+            o[x] = v;
+        } else {
+            o[x] = hw;
+        }
+    }
+    if (c->flow && bad) c->bad[y] = 1;
+}
+
+/* wmc_half_laplace, fp32 canonical; planes independent. */
+OR_EXPORT int or_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
+                             int32_t planes, int64_t plane_stride, int32_t threads) {
+    if (w <= 0 || h <= 0 || planes <= 0 || pitch < w) return 1;
+    for (int p = 0; p < planes; ++p) {
+        map32_ctx c = {in + p * plane_stride, out + p * plane_stride, w, h, pitch, 0, 0.f, NULL};
+        for_rows(h, threads, map32_row, &c);
+    }
+    return 0;
+}
+
+/* mc_flow(scheme=half_laplace), fp32 canonical, Jacobi ping-pong.
+ * Returns 0, or 3 with *bad_iter = first iteration (1-based) whose iterate
+ * holds a non-finite value.  img is updated in place
+ * (it holds U^iters on success).                                            */
+OR_EXPORT int or_flow_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                          int64_t plane_stride, int32_t iters, float dt, int32_t threads,
+                          int32_t* bad_iter) {
+    if (w <= 0 || h <= 0 || planes <= 0 || iters < 0 || pitch < w) return 1;
+    if (!(dt > 0.0f) || dt > 1.0f) return 1;
+    if (bad_iter) *bad_iter = 0;
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)pitch * (size_t)h);
+    int* bad = (int*)calloc((size_t)h, sizeof(int));
+    int rc = 0, first = 0;
+    for (int p = 0; p < planes && rc == 0; ++p) {
+        float* A = img + p * plane_stride;
+        float* B = tmp;
+        for (int t = 1; t <= iters; ++t) {
+            memset(bad, 0, sizeof(int) * (size_t)h);
+            map32_ctx c = {A, B, w, h, pitch, 1, dt, bad};
+            for_rows(h, threads, map32_row, &c);
+            float* s = A; A = B; B = s;
+            int any = 0;
+            for (int y = 0; y < h; ++y) any |= bad[y];
+            if (any) {
+                if (first == 0 || t < first) first = t;
+                rc = 3;
+                break;
+            }
+        }
+        if (A != img + p * plane_stride)
+            for (int y = 0; y < h; ++y)
+                memcpy(img + p * plane_stride + (int64_t)y * pitch, A + (int64_t)y * pitch,
+                       sizeof(float) * (size_t)w);
+    }
+    if (bad_iter) *bad_iter = first;
+    free(tmp);
+    free(bad);
+    return rc;
+}
+
+/* 8-bit widening on load: q / 255 in IEEE fp32. */
+OR_EXPORT void or_u8_to_f32(const uint8_t* in, float* out, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) out[i] = (float)in[i] / 255.0f;
+}
+
+/* ------------------------------------------------------------------------ */
+/* fp64 flow (the timed "reference CPU path" of mc_flow).                    */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const double* in;
+    double* out;
+    int w, h;
+    double dt;
+    volatile int* bad;
+} flow64_ctx;
+
+static void flow64_row(void* vctx, int y) {
+    flow64_ctx* c = (flow64_ctx*)vctx;
+    int bad = 0;
+    for (int x = 0; x < c->w; ++x) {
+        double hw = wmc_px_f64(c->in, c->w, c->h, c->w, y, x, NULL);
+        double v = c->in[(int64_t)y * c->w + x] + c->dt * hw;   /* Eq. 26 */
+        if (!isfinite(v)) bad = 1;
+        c->out[(int64_t)y * c->w + x] = v;
+    }
+    if (bad) c->bad[y] = 1;
+}
+
+OR_EXPORT int or_flow_f64(double* img, int32_t w, int32_t h, int32_t iters, double dt,
+                          int32_t threads, int32_t* bad_iter) {
+    if (w <= 0 || h <= 0 || iters < 0 || !(dt > 0.0) || dt > 1.0) return 1;
+    pthread_once(&hw_once, init_hw64);
+    if (bad_iter) *bad_iter = 0;
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)w * (size_t)h);
+    int* bad = (int*)calloc((size_t)h, sizeof(int));
+    double *A = img, *B = tmp;
+    int rc = 0;
+    for (int t = 1; t <= iters; ++t) {
+        memset(bad, 0, sizeof(int) * (size_t)h);
+        flow64_ctx c = {A, B, w, h, dt, bad};
+        for_rows(h, threads, flow64_row, &c);
+        double* s = A; A = B; B = s;
+        int any = 0;
+        for (int y = 0; y < h; ++y) any |= bad[y];
+        if (any) { if (bad_iter) *bad_iter = t; rc = 3; break; }
+    }
+    if (A != img) memcpy(img, A, sizeof(double) * (size_t)w * (size_t)h);
+    free(tmp);
+    free(bad);
+    return rc;
+}
+
+/* Naive per-pixel double loop without any shared helper: a second, direct   */
+/* transcription of Eqs. 27-28 used for SPEC acceptance criterion 2          */
+/* (SPEC.md:468): or_wmc_map_f64 must match it bit-exactly.                  */
+OR_EXPORT void or_wmc_naive_f64(const double* in, double* out, int32_t w, int32_t h) {
+    pthread_once(&hw_once, init_hw64);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double best = 0.0;
+            for (int i = 0; i < 8; ++i) {
+                double s = 0.0;
+                for (int dr = -1; dr <= 1; ++dr)
+                    for (int dc = -1; dc <= 1; ++dc) {
+                        int yy = y + dr < 0 ? 0 : (y + dr >= h ? h - 1 : y + dr);
+                        int xx = x + dc < 0 ? 0 : (x + dc >= w ? w - 1 : x + dc);
+                        s = s + HW64[i][dr + 1][dc + 1] * in[yy * w + xx];
+                    }
+                if (i == 0 || fabs(s) < fabs(best)) best = s;
+            }
+            out[y * w + x] = best;
+        }
+}

@@ -1,0 +1,118 @@
+/*
+ * oracle/wmc_px.h -- per-pixel restatements shared by the oracle's C
+ * (wmc_oracle.c) and C++ (ref_exec.cpp) translation units.
+ * TEST INFRASTRUCTURE ONLY (see wmc_oracle.c header).
+ */
+#ifndef CF_ORACLE_WMC_PX_H
+#define CF_ORACLE_WMC_PX_H
+#include <math.h>
+#include <stdint.h>
+#include <pthread.h>
+
+static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* ------------------------------------------------------------------------ */
+/* Kernel bank h1..h8.  Stored as exact   */
+/* integer numerators over 12, lowered to double once.         */
+/* Index [i][row][col], row = dy+1 (top to bottom), col = dx+1 (left to      */
+/* right) -- the Stencil3 orientation of SPEC.md:41 / :77.                   */
+/* ------------------------------------------------------------------------ */
+static const int H12[8][3][3] = {
+    /* h1 left half   */ {{2, 2, 0}, {4, -12, 0}, {2, 2, 0}},
+    /* h2 top half    */ {{2, 4, 2}, {2, -12, 2}, {0, 0, 0}},
+    /* h3 right half  */ {{0, 2, 2}, {0, -12, 4}, {0, 2, 2}},
+    /* h4 bottom half */ {{0, 0, 0}, {2, -12, 2}, {2, 4, 2}},
+    /* h5 upper-left  */ {{2, 4, 1}, {4, -12, 0}, {1, 0, 0}},
+    /* h6 upper-right */ {{1, 4, 2}, {0, -12, 4}, {0, 0, 1}},
+    /* h7 lower-right */ {{0, 0, 1}, {0, -12, 4}, {1, 4, 2}},
+    /* h8 lower-left  */ {{1, 0, 0}, {4, -12, 0}, {2, 4, 1}},
+};
+
+static inline void kernel_bank_numerators(int32_t* out72) {
+    for (int i = 0; i < 8; ++i)
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) out72[i * 9 + r * 3 + c] = H12[i][r][c];
+}
+
+static double HW64[8][3][3];
+static pthread_once_t hw_once = PTHREAD_ONCE_INIT;
+static void init_hw64(void) {
+    for (int i = 0; i < 8; ++i)
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                int n = H12[i][r][c];
+                /* exact rationals: n/12 reduced -> 1/6, 1/3, 1/12, -1, 0 */
+                HW64[i][r][c] = n == 0 ? 0.0 : (n == -12 ? -1.0 : (double)n / 12.0);
+            }
+}
+
+static inline double wmc_px_f64(const double* in, int w, int h, int64_t pitch, int y, int x,
+                                int* m_out) {
+    double d[8];
+    for (int i = 0; i < 8; ++i) {
+        double s = 0.0;
+        for (int r = 0; r < 3; ++r) {          /* SPEC.md:56 correlation, row-major taps */
+            int yy = clampi(y + r - 1, 0, h - 1);   /* clamp-to-edge */
+            const double* row = in + (int64_t)yy * pitch;
+            for (int c = 0; c < 3; ++c) {
+                int xx = clampi(x + c - 1, 0, w - 1);
+                s = s + HW64[i][r][c] * row[xx];
+            }
+        }
+        d[i] = s;
+    }
+    int m = 0;                                   /* SPEC.md:173, :195 strict <, first min */
+    for (int i = 1; i < 8; ++i)
+        if (fabs(d[i]) < fabs(d[m])) m = i;
+    if (m_out) *m_out = m;
+    return d[m];
+}
+
+/* ------------------------------------------------------------------------ */
+/* fp32 canonical evaluation, every rounding pinned.  */
+/*                                                                           */
+/*   a b c        12*d1 = 2((a+e)+(b+f)) + 4l - 12u       (h1)               */
+/*   l u r        12*d2 = 2((a+c)+(l+r)) + 4b - 12u       (h2)               */
+/*   e f g        12*d3 = 2((b+f)+(c+g)) + 4r - 12u       (h3)               */
+/*                12*d4 = 2((l+r)+(e+g)) + 4f - 12u       (h4)               */
+/*                12*d5 = 4(b+l) + 2a + (c+e) - 12u       (h5)               */
+/*                12*d6 = 4(b+r) + 2c + (a+g) - 12u       (h6)               */
+/*                12*d7 = 4(r+f) + 2g + (c+e) - 12u       (h7)               */
+/*                12*d8 = 4(l+f) + 2e + (a+g) - 12u       (h8)               */
+/*                                                                           */
+/* ×2 and ×4 are exact, so fmaf(2,x,y) is the single rounding of 2x+y.       */
+/* n12u = fl(u * -12) is formed once and ADDED, so a constant image gives    */
+/* exact zeros (fl(2*fl(6u)) == fl(12u)).  D_m selected by strict < on |D|   */
+/* scanning 1..8; H^w = fl(D_m * fl(1/12)); flow step fmaf(dt, H^w, u).       */
+/* ------------------------------------------------------------------------ */
+static const float C12 = 1.0f / 12.0f; /* fl(1/12) = 0x3DAAAAAB */
+
+static inline float wmc_px_f32(float a, float b, float c, float l, float u, float r, float e,
+                               float f, float g) {
+    const float n12u = u * -12.0f;
+    const float Vl = a + e, Vc = b + f, Vr = c + g;
+    const float Wm = Vl + Vc, W0 = Vc + Vr;
+    const float Ht = a + c, Hc = l + r, Hb = e + g;
+    const float Tm = Ht + Hc, T0 = Hc + Hb;
+    const float D1 = fmaf(2.0f, fmaf(2.0f, l, Wm), n12u);
+    const float D2 = fmaf(2.0f, fmaf(2.0f, b, Tm), n12u);
+    const float D3 = fmaf(2.0f, fmaf(2.0f, r, W0), n12u);
+    const float D4 = fmaf(2.0f, fmaf(2.0f, f, T0), n12u);
+    const float K5 = c + e, K6 = a + g;
+    const float Pbl = b + l, Pbr = b + r, Prf = r + f, Plf = l + f;
+    const float D5 = fmaf(4.0f, Pbl, fmaf(2.0f, a, K5)) + n12u;
+    const float D6 = fmaf(4.0f, Pbr, fmaf(2.0f, c, K6)) + n12u;
+    const float D7 = fmaf(4.0f, Prf, fmaf(2.0f, g, K5)) + n12u;
+    const float D8 = fmaf(4.0f, Plf, fmaf(2.0f, e, K6)) + n12u;
+    float best = D1;
+    if (fabsf(D2) < fabsf(best)) best = D2;
+    if (fabsf(D3) < fabsf(best)) best = D3;
+    if (fabsf(D4) < fabsf(best)) best = D4;
+    if (fabsf(D5) < fabsf(best)) best = D5;
+    if (fabsf(D6) < fabsf(best)) best = D6;
+    if (fabsf(D7) < fabsf(best)) best = D7;
+    if (fabsf(D8) < fabsf(best)) best = D8;
+    return best * C12;
+}
+
+#endif

@@ -1,0 +1,20 @@
+"""curveflow-b200: B200-native (sm_100a) discrete weighted-mean-curvature map and
+WMC flow filter of Gong & Goksel, arXiv 1903.07189.
+
+Drop-in for the reference's ``wmc_half_laplace`` / ``mc_flow`` (SPEC.md:171,
+:256): C-ABI in include/curveflow/capi.h, C++ API in include/curveflow/wmc.hpp,
+this Python mirror in :mod:`.curveflow`.
+"""
+from .curveflow import (FlowConfig, FlowError, kernel, kernel_bank, max_sweeps_per_launch,
+                        mc_flow, mc_flow_u8, merge_channels, split_channels, sweeps_band,
+                        synth_image, wmc_half_laplace, workspace_bytes)
+from ._lib import LIB_PATH, CurveflowError, CurveflowLibraryError, lib
+from .configs import CONFIGS, WmcConfig
+
+__all__ = [
+    "FlowConfig", "FlowError", "kernel", "kernel_bank", "max_sweeps_per_launch", "mc_flow",
+    "mc_flow_u8", "merge_channels", "split_channels", "sweeps_band", "synth_image",
+    "wmc_half_laplace", "workspace_bytes", "LIB_PATH", "CurveflowError",
+    "CurveflowLibraryError", "lib", "CONFIGS", "WmcConfig",
+]
+__version__ = "0.1.0"

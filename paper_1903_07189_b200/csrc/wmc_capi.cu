@@ -1,0 +1,368 @@
+// paper_1903_07189_b200/csrc/wmc_capi.cu -- host side of the C-ABI
+// (include/curveflow/capi.h): validation, launch planning, ping-pong
+// scheduling of the temporally blocked flow, non-finite flag plumbing.
+//
+// Reference interfaces replaced (the SPEC operations on the path; the
+// reference ships no code for them): wmc_half_laplace SPEC.md:171-179,
+// mc_flow(scheme=half_laplace) SPEC.md:256-272.
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/curveflow/capi.h"
+#include "wmc_sweep.cuh"
+
+namespace {
+
+constexpr int kMaxLevels = 4;            // sweeps fused per launch
+constexpr int kC = 4;                    // columns per lane
+constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
+constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
+
+thread_local int g_last_cuda = 0;
+
+int cuda_fail(cudaError_t e) {
+    g_last_cuda = (int)e;
+    return CF_ECUDA;
+}
+#define CF_CUDA(x)                                  \
+    do {                                            \
+        cudaError_t e_ = (x);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_); \
+    } while (0)
+
+struct DevInfo {
+    int sms = 0;
+    int cc_major = 0, cc_minor = 0;
+};
+
+std::mutex g_dev_mu;
+std::vector<DevInfo> g_dev;
+
+int device_info(DevInfo* out) {
+    int dev = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+    DevInfo& d = g_dev[dev];
+    if (d.sms == 0) {
+        CF_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+        CF_CUDA(cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+        CF_CUDA(cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+    }
+    if (d.cc_major != 10 || d.cc_minor != 0) return CF_ENODEV;
+    *out = d;
+    return CF_OK;
+}
+
+template <int K, bool MAP, bool VEC, bool U8>
+int kernel_occupancy_warps() {
+    static int cached = -1;  // per instantiation; identical on every B200
+    if (cached < 0) {
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &blocks, cfk::wmc_sweeps_kernel<kC, K, MAP, VEC, U8>, cfk::kThreads, 0) !=
+                cudaSuccess ||
+            blocks <= 0)
+            blocks = 2;
+        cached = blocks * cfk::kWarpsPerBlock;
+    }
+    return cached;
+}
+
+// Strip planner: choose rows per warp-task so that the number of waves times
+// the per-task length (rows + temporal warm-up + fixed cost) is minimal.
+void plan_strips(cfk::SweepParams& p, int K, int slots) {
+    const int rows = p.y1 - p.y0;
+    const int64_t per_strip_tasks = (int64_t)p.n_chunks * p.planes;
+    const double overhead = (K - 1) + 6.0;  // warm-up rows + fixed per-task cost (rows)
+    const int max_strips = std::max(1, rows / std::max(8, 4 * K));
+    double best_cost = 1e300;
+    int best = 1;
+    for (int ns = 1; ns <= max_strips; ++ns) {
+        const int sr = (rows + ns - 1) / ns;
+        const int ns_eff = (rows + sr - 1) / sr;
+        const int64_t tasks = per_strip_tasks * ns_eff;
+        const int64_t waves = (tasks + slots - 1) / slots;
+        const double cost = (double)waves * (sr + overhead);
+        if (cost < best_cost * 0.999) { best_cost = cost; best = ns; }
+        if (tasks > (int64_t)slots * 64) break;
+    }
+    p.strip_rows = (rows + best - 1) / best;
+    p.n_strips = (rows + p.strip_rows - 1) / p.strip_rows;
+}
+
+template <int K, bool MAP, bool VEC, bool U8>
+int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
+    using G = cfk::Geo<kC, K>;
+    p.n_chunks = (p.w + G::S - 1) / G::S;
+    plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MAP, VEC, U8>());
+    const int64_t tasks = (int64_t)p.n_chunks * p.n_strips * p.planes;
+    const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
+    if (blocks > INT_MAX) return CF_EINVAL;
+    cfk::wmc_sweeps_kernel<kC, K, MAP, VEC, U8><<<(unsigned)blocks, cfk::kThreads, 0, s>>>(p);
+    CF_CUDA(cudaGetLastError());
+    return CF_OK;
+}
+
+template <bool MAP, bool VEC, bool U8>
+int launch(const cfk::SweepParams& p, int K, const DevInfo& d, cudaStream_t s) {
+    if constexpr (MAP) {
+        return launch_k<1, true, VEC, U8>(p, d, s);
+    } else {
+        switch (K) {
+            case 1: return launch_k<1, false, VEC, U8>(p, d, s);
+            case 2: return launch_k<2, false, VEC, U8>(p, d, s);
+            case 3: return launch_k<3, false, VEC, U8>(p, d, s);
+            case 4: return launch_k<4, false, VEC, U8>(p, d, s);
+            default: return CF_EINVAL;
+        }
+    }
+}
+
+bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
+
+bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane_stride) {
+    if (w <= 0 || h <= 0 || planes <= 0 || pitch < w) return false;
+    if (planes > 1 && plane_stride < pitch * (int64_t)h) return false;
+    if ((int64_t)w > (1 << 30) || (int64_t)h > (1 << 30)) return false;
+    return true;
+}
+
+// Launch schedule: sweeps per launch, at most kMaxLevels each, an EVEN number
+// of launches when iters >= 2 so the ping-pong ends in the caller's buffer.
+std::vector<int> schedule(int iters) {
+    std::vector<int> ks;
+    int left = iters;
+    while (left > 0) {
+        const int k = std::min(left, kMaxLevels);
+        ks.push_back(k);
+        left -= k;
+    }
+    if (ks.size() % 2 == 1 && iters >= 2) {
+        // split the largest launch (>= 2 sweeps) into two
+        auto it = std::max_element(ks.begin(), ks.end());
+        const int k = *it;
+        *it = k / 2;
+        ks.insert(it + 1, k - k / 2);
+    }
+    return ks;
+}
+
+__global__ void u8_to_f32_kernel(const uint8_t* in, int64_t in_pitch, int64_t in_plane, float* out,
+                                 int64_t pitch, int64_t plane, int32_t w, int32_t h) {
+    const int64_t n = (int64_t)w * h;
+    const int p = blockIdx.y;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = i / w, x = i % w;
+        out[p * plane + y * pitch + x] =
+            __fdiv_rn((float)in[p * in_plane + y * in_pitch + x], 255.0f);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+CF_API const char* cf_version(void) { return "curveflow-b200 0.1.0 (sm_100a)"; }
+
+CF_API const char* cf_status_string(int status) {
+    switch (status) {
+        case CF_OK: return "ok";
+        case CF_EINVAL: return "invalid argument (shape, pitch, planes, iters, dt or workspace)";
+        case CF_ECUDA: return "CUDA runtime error";
+        case CF_ENONFINITE: return "non-finite value produced (instability)";
+        case CF_ENODEV: return "no sm_100 (B200) device";
+        default: return "unknown status";
+    }
+}
+
+CF_API int cf_last_cuda_error(void) { return g_last_cuda; }
+
+CF_API int32_t cf_wmc_max_sweeps_per_launch(void) { return kMaxLevels; }
+
+CF_API void cf_kernel_bank_x12(int32_t* out72) {
+    // PAPER.md:411-444; SPEC.md:96-111 -- h_i * 12, [i][row][col]
+    static const int32_t H12[72] = {
+        2, 2, 0, 4, -12, 0, 2, 2, 0,    // h1
+        2, 4, 2, 2, -12, 2, 0, 0, 0,    // h2
+        0, 2, 2, 0, -12, 4, 0, 2, 2,    // h3
+        0, 0, 0, 2, -12, 2, 2, 4, 2,    // h4
+        2, 4, 1, 4, -12, 0, 1, 0, 0,    // h5
+        1, 4, 2, 0, -12, 4, 0, 0, 1,    // h6
+        0, 0, 1, 0, -12, 4, 1, 4, 2,    // h7
+        1, 0, 0, 4, -12, 0, 2, 4, 1,    // h8
+    };
+    std::memcpy(out72, H12, sizeof(H12));
+}
+
+CF_API int cf_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
+                          int32_t planes, int64_t plane_stride, void* stream) {
+    if (!in || !out || in == out || !shape_ok(w, h, pitch, planes, plane_stride)) return CF_EINVAL;
+    DevInfo d;
+    if (int rc = device_info(&d)) return rc;
+    cfk::SweepParams p{};
+    p.src = in; p.dst = out;
+    p.src_pitch = p.dst_pitch = pitch;
+    p.src_plane = p.dst_plane = plane_stride;
+    p.src_row0 = p.dst_row0 = 0;
+    p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
+    p.dt = 0.f; p.iter_base = 0; p.flag = nullptr;
+    const bool vec = pitch % 4 == 0 && (planes == 1 || plane_stride % 4 == 0) && aligned16(in) &&
+                     aligned16(out);
+    cudaStream_t s = (cudaStream_t)stream;
+    return vec ? launch<true, true, false>(p, 1, d, s) : launch<true, false, false>(p, 1, d, s);
+}
+
+CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                                            int64_t plane_stride) {
+    if (!shape_ok(w, h, pitch, planes, plane_stride)) return 0;
+    const int64_t elems = (planes - 1) * (planes > 1 ? plane_stride : 0) + pitch * (int64_t)h;
+    return kWsHeader + (size_t)elems * sizeof(float);
+}
+
+static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t src_plane,
+                    float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                    int64_t plane_stride, int32_t iters, float dt, void* workspace,
+                    size_t ws_bytes, int32_t* first_bad_iter, cudaStream_t s) {
+    DevInfo d;
+    if (int rc = device_info(&d)) return rc;
+    int32_t* flag = reinterpret_cast<int32_t*>(workspace);
+    float* ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kWsHeader);
+    CF_CUDA(cudaMemsetAsync(flag, 0x7f, sizeof(int32_t), s));
+
+    const std::vector<int> ks = schedule(iters);
+    const bool vec_out = pitch % 4 == 0 && (planes == 1 || plane_stride % 4 == 0) &&
+                         aligned16(out) && aligned16(ws);
+    // Ping-pong targets.  f32: src0 == out, the first launch writes ws.
+    // u8: src0 is separate; choose the first target so the last lands in out.
+    float* buf[2] = {ws, out};
+    int tgt = 0;
+    if (src_u8) tgt = (ks.size() % 2 == 1) ? 1 : 0;
+
+    const void* cur = src0;
+    bool cur_u8 = src_u8;
+    int64_t cur_pitch = src_pitch, cur_plane = src_plane;
+    int iter = 0;
+    for (size_t i = 0; i < ks.size(); ++i) {
+        float* dst = buf[tgt];
+        cfk::SweepParams p{};
+        p.src = cur; p.dst = dst;
+        p.src_pitch = cur_pitch; p.dst_pitch = pitch;
+        p.src_plane = cur_plane; p.dst_plane = plane_stride;
+        p.src_row0 = p.dst_row0 = 0;
+        p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
+        p.dt = dt; p.iter_base = iter; p.flag = flag;
+        int rc;
+        if (cur_u8) {
+            const bool vec = vec_out && cur_pitch % 4 == 0 && (planes == 1 || cur_plane % 4 == 0) &&
+                             ((uintptr_t)cur & 3u) == 0;
+            rc = vec ? launch<false, true, true>(p, ks[i], d, s)
+                     : launch<false, false, true>(p, ks[i], d, s);
+        } else {
+            const bool vec = vec_out && aligned16(cur);
+            rc = vec ? launch<false, true, false>(p, ks[i], d, s)
+                     : launch<false, false, false>(p, ks[i], d, s);
+        }
+        if (rc) return rc;
+        iter += ks[i];
+        cur = dst; cur_u8 = false; cur_pitch = pitch; cur_plane = plane_stride;
+        tgt ^= 1;
+    }
+    if (!src_u8 && iters == 1) {
+        // single launch wrote ws: copy U^1 back into the caller's buffer
+        for (int pl = 0; pl < planes; ++pl)
+            CF_CUDA(cudaMemcpy2DAsync(out + pl * plane_stride, pitch * 4, ws + pl * plane_stride,
+                                      pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
+    }
+    if (first_bad_iter) return cf_wmc_filter_query_nonfinite(workspace, first_bad_iter, s);
+    (void)ws_bytes;
+    return CF_OK;
+}
+
+CF_API int cf_wmc_filter_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                             int64_t plane_stride, int32_t iters, float dt, void* workspace,
+                             size_t workspace_bytes, int32_t* first_bad_iter, void* stream) {
+    if (!img || !shape_ok(w, h, pitch, planes, plane_stride) || iters < 0) return CF_EINVAL;
+    if (!(dt > 0.0f) || dt > 1.0f) return CF_EINVAL;
+    if (first_bad_iter) *first_bad_iter = 0;
+    if (iters == 0) return CF_OK;                     // identity
+    if (!workspace ||
+        workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))
+        return CF_EINVAL;
+    return run_flow(img, false, pitch, plane_stride, img, w, h, pitch, planes, plane_stride,
+                    iters, dt, workspace, workspace_bytes, first_bad_iter,
+                    (cudaStream_t)stream);
+}
+
+CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
+                                float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                                int64_t plane_stride, int32_t iters, float dt, void* workspace,
+                                size_t workspace_bytes, int32_t* first_bad_iter, void* stream) {
+    if (!in || !out || !shape_ok(w, h, pitch, planes, plane_stride) || iters < 0)
+        return CF_EINVAL;
+    if (in_pitch < w || (planes > 1 && in_plane_stride < in_pitch * (int64_t)h)) return CF_EINVAL;
+    if (!(dt > 0.0f) || dt > 1.0f) return CF_EINVAL;
+    if (first_bad_iter) *first_bad_iter = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (iters == 0) {
+        dim3 grid(1184, planes);
+        u8_to_f32_kernel<<<grid, 256, 0, s>>>(in, in_pitch, in_plane_stride, out, pitch,
+                                               plane_stride, w, h);
+        CF_CUDA(cudaGetLastError());
+        return CF_OK;
+    }
+    if (!workspace ||
+        workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))
+        return CF_EINVAL;
+    return run_flow(in, true, in_pitch, in_plane_stride, out, w, h, pitch, planes, plane_stride,
+                    iters, dt, workspace, workspace_bytes, first_bad_iter, s);
+}
+
+CF_API int cf_wmc_filter_query_nonfinite(const void* workspace, int32_t* first_bad_iter,
+                                         void* stream) {
+    if (!workspace || !first_bad_iter) return CF_EINVAL;
+    int32_t host = kFlagNone;
+    cudaStream_t s = (cudaStream_t)stream;
+    CF_CUDA(cudaMemcpyAsync(&host, workspace, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaStreamSynchronize(s));
+    if (host >= kFlagNone || host <= 0) {
+        *first_bad_iter = 0;
+        return CF_OK;
+    }
+    *first_bad_iter = host;
+    return CF_ENONFINITE;
+}
+
+CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,
+                                  float* dst, int32_t dst_row0, int32_t w, int32_t h,
+                                  int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,
+                                  float dt, int32_t iter_base, int32_t* d_flag, void* stream) {
+    if (!src || !dst || w <= 0 || h <= 0 || pitch < w) return CF_EINVAL;
+    if (sweeps < 1 || sweeps > kMaxLevels || !(dt > 0.0f) || dt > 1.0f) return CF_EINVAL;
+    if (y0 < 0 || y1 > h || y0 >= y1) return CF_EINVAL;
+    const int need0 = std::max(0, y0 - sweeps), need1 = std::min(h, y1 + sweeps);
+    if (src_row0 > need0 || src_row0 + src_rows < need1) return CF_EINVAL;
+    DevInfo d;
+    if (int rc = device_info(&d)) return rc;
+    cfk::SweepParams p{};
+    p.src = src; p.dst = dst;
+    p.src_pitch = p.dst_pitch = pitch;
+    p.src_plane = p.dst_plane = 0;
+    p.src_row0 = src_row0; p.dst_row0 = dst_row0;
+    p.w = w; p.h = h; p.y0 = y0; p.y1 = y1; p.planes = 1;
+    p.dt = dt; p.iter_base = iter_base; p.flag = d_flag;
+    const bool vec = pitch % 4 == 0 && aligned16(src) && aligned16(dst);
+    cudaStream_t s = (cudaStream_t)stream;
+    return vec ? launch<false, true, false>(p, sweeps, d, s)
+               : launch<false, false, false>(p, sweeps, d, s);
+}
+
+}  // extern "C"

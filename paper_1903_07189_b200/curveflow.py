@@ -1,0 +1,269 @@
+"""Host-side mirror of the reference's operator interface for the WMC path.
+
+The reference (arXiv 1903.07189; /root/reference/SPEC.md) defines, in namespace
+``curveflow``:
+
+* ``wmc_half_laplace(img: Image2D) -> Image2D``
+* ``mc_flow(img: Image2D, cfg: FlowConfig) -> Image2D``
+* ``FlowConfig{dt, iters, scheme}``
+* ``kernel(name)`` / ``KernelBank`` (h1..h8)
+* ``split_channels`` / ``merge_channels``
+
+Same names, argument meaning and error behaviour here; the arithmetic runs in
+the sm_100a kernels of ``libcurveflow_b200.so`` through the C-ABI
+(include/curveflow/capi.h).  There is no CPU fallback: every call needs the
+native library and a B200.
+
+Images are ``torch.Tensor`` (CUDA, float32, shape (H, W) or (P, H, W) for P
+channel planes) or ``numpy.ndarray`` (host; copied to the device and back --
+the end-to-end path).  Values are real intensities (the reference's 0-255
+scale or [0, 1]; the operator is homogeneous).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from ._lib import CF_ENONFINITE, check, lib
+
+__all__ = [
+    "FlowConfig", "FlowError", "wmc_half_laplace", "mc_flow", "mc_flow_u8", "kernel",
+    "kernel_bank", "split_channels", "merge_channels", "synth_image", "sweeps_band",
+    "max_sweeps_per_launch", "workspace_bytes",
+]
+
+_HALF = ("h1", "h2", "h3", "h4", "h5", "h6", "h7", "h8")
+
+
+class FlowError(RuntimeError):
+    """mc_flow instability: a non-finite value appeared."""
+
+    def __init__(self, iteration: int):
+        super().__init__(f"mc_flow: non-finite value at iteration {iteration}")
+        self.iteration = iteration
+
+
+@dataclass(frozen=True)
+class FlowConfig:
+    """SPEC.md:250-253.  dt default 1.0 for half_laplace; dt <= 1."""
+
+    dt: float = 1.0
+    iters: int = 0
+    scheme: str = "half_laplace"
+
+    def validate(self) -> None:
+        if self.scheme not in ("half_laplace", "half"):
+            raise NotImplementedError(
+                "scheme='fd' (central-difference WMC, SPEC.md:163-170) is outside this "
+                "build's hot path; only scheme='half_laplace' is provided")
+        if not (self.dt > 0.0) or self.dt > 1.0:
+            raise ValueError("FlowConfig.dt must satisfy 0 < dt <= 1 for half_laplace "
+                             "(SPEC.md:252)")
+        if int(self.iters) != self.iters or self.iters < 0:
+            raise ValueError("FlowConfig.iters must be a nonnegative integer")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(torch, dev) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _as_planes(t):
+    """(H, W) -> (1, H, W); (P, H, W) stays.  Returns (tensor3d, squeeze)."""
+    if t.dim() == 2:
+        return t.unsqueeze(0), True
+    if t.dim() == 3:
+        return t, False
+    raise ValueError("image must be (H, W) or (P, H, W)")
+
+
+def _device_image(img):
+    torch = _torch()
+    if isinstance(img, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda(), True
+    if not isinstance(img, torch.Tensor):
+        raise TypeError("image must be a torch.Tensor or numpy.ndarray")
+    if not img.is_cuda:
+        return img.to(dtype=torch.float32).contiguous().cuda(), True
+    if img.dtype != torch.float32:
+        raise TypeError("device images must be float32")
+    return img, False
+
+
+def wmc_half_laplace(img):
+    """Discrete WMC map d_m; returns a new image."""
+    torch = _torch()
+    src, host = _device_image(img)
+    x, squeeze = _as_planes(src)
+    x = x if x.stride(-1) == 1 else x.contiguous()
+    P, H, W = x.shape
+    out = torch.empty((P, H, W), dtype=torch.float32, device=x.device)
+    if P and H and W:
+        pitch, plane = x.stride(1), x.stride(0)
+        if out.stride(1) != pitch or out.stride(0) != plane:
+            x = x.contiguous()
+            pitch, plane = x.stride(1), x.stride(0)
+        with torch.cuda.device(x.device):
+            check(lib().cf_wmc_map_f32(x.data_ptr(), out.data_ptr(), W, H, pitch, P, plane,
+                                       _stream_ptr(torch, x.device)), "wmc_half_laplace")
+    res = out[0] if squeeze else out
+    if host:
+        return res.cpu().numpy() if isinstance(img, np.ndarray) else res.cpu()
+    return res
+
+
+def workspace_bytes(h: int, w: int, planes: int = 1) -> int:
+    return int(lib().cf_wmc_filter_workspace_bytes(w, h, w, planes, w * h))
+
+
+def mc_flow(img, cfg: FlowConfig, *, check_finite: bool = True, workspace=None,
+            inplace: bool = False):
+    """Mean-curvature flow, scheme=half_laplace.
+
+    Returns U^iters.  Raises FlowError(iteration) if an iterate becomes
+    non-finite.  ``inplace=True`` (device tensors only)
+    overwrites ``img``.  ``check_finite=False`` skips the host sync the
+    diagnostic needs (the device-side check still runs).
+    """
+    torch = _torch()
+    cfg.validate()
+    src, host = _device_image(img)
+    if inplace and (host or not src.is_contiguous()):
+        raise ValueError("inplace=True needs a contiguous CUDA tensor")
+    x = src if inplace else src.clone(memory_format=torch.contiguous_format)
+    x3, squeeze = _as_planes(x)
+    P, H, W = x3.shape
+    if cfg.iters > 0 and P and H and W:
+        nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = torch.empty(nbytes, dtype=torch.uint8, device=x3.device)
+        bad = C.c_int32(0)
+        with torch.cuda.device(x3.device):
+            rc = lib().cf_wmc_filter_f32(x3.data_ptr(), W, H, W, P, H * W, int(cfg.iters),
+                                         float(cfg.dt), workspace.data_ptr(), nbytes,
+                                         C.byref(bad) if check_finite else None,
+                                         _stream_ptr(torch, x3.device))
+        if rc == CF_ENONFINITE:
+            raise FlowError(bad.value)
+        check(rc, "mc_flow")
+    res = x3[0] if squeeze else x3
+    if host:
+        return res.cpu().numpy() if isinstance(img, np.ndarray) else res.cpu()
+    return res
+
+
+def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=None, out=None):
+    """8-bit input widened on device as q/255 (BASELINE cfg 5), then
+    mc_flow; returns float32 U^iters of the same (P, H, W) / (H, W) shape."""
+    torch = _torch()
+    cfg.validate()
+    if isinstance(img_u8, np.ndarray):
+        src = torch.from_numpy(np.ascontiguousarray(img_u8, dtype=np.uint8)).cuda()
+        host = True
+    else:
+        src, host = img_u8.contiguous(), not img_u8.is_cuda
+        if host:
+            src = src.cuda()
+    if src.dtype != torch.uint8:
+        raise TypeError("mc_flow_u8 expects uint8 input")
+    s3, squeeze = _as_planes(src)
+    P, H, W = s3.shape
+    if out is None:
+        out = torch.empty((P, H, W), dtype=torch.float32, device=s3.device)
+    nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+    if cfg.iters > 0 and (workspace is None or workspace.numel() < nbytes):
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=s3.device)
+    bad = C.c_int32(0)
+    with torch.cuda.device(s3.device):
+        rc = lib().cf_wmc_filter_u8_f32(
+            s3.data_ptr(), W, H * W, out.data_ptr(), W, H, W, P, H * W, int(cfg.iters),
+            float(cfg.dt), workspace.data_ptr() if workspace is not None else None,
+            nbytes if workspace is not None else 0, C.byref(bad) if check_finite else None,
+            _stream_ptr(torch, s3.device))
+    if rc == CF_ENONFINITE:
+        raise FlowError(bad.value)
+    check(rc, "mc_flow_u8")
+    res = out[0] if squeeze else out
+    if host:
+        return res.cpu().numpy() if isinstance(img_u8, np.ndarray) else res.cpu()
+    return res
+
+
+def max_sweeps_per_launch() -> int:
+    return int(lib().cf_wmc_max_sweeps_per_launch())
+
+
+def sweeps_band(src, src_row0: int, dst, dst_row0: int, h: int, y0: int, y1: int, sweeps: int,
+                dt: float, iter_base: int, flag=None) -> None:
+    """Row-band primitive (C-ABI cf_wmc_sweeps_band_f32): `sweeps` fused Jacobi
+    sweeps producing global rows [y0, y1) of a height-h image from a band buffer
+    `src` holding global rows [src_row0, src_row0 + src.shape[0])."""
+    torch = _torch()
+    assert src.is_cuda and dst.is_cuda and src.dtype == torch.float32 and src.is_contiguous()
+    W = src.shape[1]
+    with torch.cuda.device(src.device):
+        check(lib().cf_wmc_sweeps_band_f32(
+            src.data_ptr(), src_row0, src.shape[0], dst.data_ptr(), dst_row0, W, h, W, y0, y1,
+            sweeps, float(dt), iter_base, flag.data_ptr() if flag is not None else None,
+            _stream_ptr(torch, src.device)), "sweeps_band")
+
+
+def kernel_bank() -> dict:
+    """h1..h8 as exact rationals, [row][col]."""
+    buf = (C.c_int32 * 72)()
+    lib().cf_kernel_bank_x12(buf)
+    bank = {}
+    for i, name in enumerate(_HALF):
+        bank[name] = [[Fraction(buf[i * 9 + r * 3 + c], 12) for c in range(3)] for r in range(3)]
+    return bank
+
+
+def kernel(name: str):
+    """SPEC.md:105 kernel(name) for the half-Laplace kernels h1..h8."""
+    bank = kernel_bank()
+    if name not in bank:
+        raise KeyError(f"kernel {name!r}: this build carries h1..h8 (the hot path); "
+                       "the Laplace diagnostics k1..k4 are out of scope")
+    return bank[name]
+
+
+def split_channels(img: np.ndarray):
+    """(H, W) -> [plane]; (H, W, 3) -> 3 planes; else format error."""
+    a = np.asarray(img)
+    if a.ndim == 2:
+        return [a]
+    if a.ndim == 3 and a.shape[2] == 3:
+        return [np.ascontiguousarray(a[:, :, c]) for c in range(3)]
+    raise ValueError("unsupported channel count (SPEC.md:65): expected 1 or 3")
+
+
+def merge_channels(planes):
+    if len(planes) == 1:
+        return np.asarray(planes[0])
+    if len(planes) == 3:
+        return np.stack([np.asarray(p) for p in planes], axis=2)
+    raise ValueError("unsupported channel count (SPEC.md:65): expected 1 or 3")
+
+
+def synth_image(h: int, w: int, seed: int, n_rects: int, n_discs: int, sigma: float,
+                dtype: str = "f32", threads: int = 0) -> np.ndarray:
+    """Seeded synthetic image (host), DESIGN.md §6 / csrc/synth.cpp."""
+    if dtype == "f32":
+        out = np.empty((h, w), dtype=np.float32)
+        fn = lib().cf_synth_f32
+    elif dtype == "u8":
+        out = np.empty((h, w), dtype=np.uint8)
+        fn = lib().cf_synth_u8
+    else:
+        raise ValueError("dtype must be 'f32' or 'u8'")
+    check(fn(out.ctypes.data, w, h, w, int(seed) & (2**64 - 1), n_rects, n_discs, float(sigma),
+             threads), "synth_image")
+    return out
+

@@ -1,0 +1,131 @@
+"""GPU parity: the sm_100a kernels through the C-ABI vs the fp32 canonical
+oracle (bit-exact) and the fp64 SPEC-faithful oracle (<= 1e-5)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1903_07189_b200 as cf
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def assert_bitexact(got, ref, what=""):
+    g, r = bits(got), bits(ref)
+    if not np.array_equal(g, r):
+        d = np.argwhere(g != r)
+        i = tuple(d[0])
+        raise AssertionError(f"{what}: {len(d)} mismatches, first at {i}: "
+                             f"got {np.asarray(got)[i]!r} ref {np.asarray(ref)[i]!r}")
+
+
+SHAPES = [(1, 1), (1, 7), (7, 1), (2, 2), (3, 3), (17, 31), (31, 17), (5, 119), (5, 120),
+          (5, 121), (9, 124), (33, 128), (64, 240), (67, 241), (130, 361), (257, 512)]
+
+
+@pytest.mark.parametrize("h,w", SHAPES)
+def test_map_bitexact_shapes(h, w):
+    img = cf.synth_image(h, w, seed=h * 1000 + w, n_rects=3, n_discs=3, sigma=0.1)
+    got = cf.wmc_half_laplace(torch.from_numpy(img).cuda()).cpu().numpy()
+    assert_bitexact(got, oracle.wmc_map_f32(img), f"map {h}x{w}")
+
+
+def test_map_vs_fp64_cfg1():
+    c = cf.CONFIGS["cfg1"]
+    img = cf.synth_image(c.h, c.w, c.seed(0), c.n_rects, c.n_discs, c.sigma)
+    got = cf.wmc_half_laplace(torch.from_numpy(img).cuda()).cpu().numpy()
+    ref64 = oracle.wmc_map_f64(img.astype(np.float64))
+    assert np.abs(got.astype(np.float64) - ref64).max() <= 1e-5   # north_star tolerance
+    assert_bitexact(got, oracle.wmc_map_f32(img), "cfg1 map")
+
+
+def test_map_planes_and_pitch():
+    imgs = np.stack([cf.synth_image(45, 77, seed=s, n_rects=3, n_discs=3, sigma=0.1)
+                     for s in range(3)])
+    got = cf.wmc_half_laplace(torch.from_numpy(imgs).cuda()).cpu().numpy()
+    assert_bitexact(got, oracle.wmc_map_f32(imgs), "planes")
+    # padded pitch (vector path needs pitch % 4 == 0; 77 -> 80)
+    big = torch.zeros((3, 45, 80), device="cuda")
+    big[:, :, :77] = torch.from_numpy(imgs).cuda()
+    view = big[:, :, :77]
+    got2 = cf.wmc_half_laplace(view).cpu().numpy()
+    assert_bitexact(got2, oracle.wmc_map_f32(imgs), "pitched")
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3, 4, 5, 7, 8, 9, 13, 100])
+def test_flow_bitexact_iters(iters):
+    img = cf.synth_image(97, 203, seed=iters, n_rects=5, n_discs=5, sigma=0.1)
+    got = cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(dt=1.0, iters=iters))
+    ref, bad = oracle.flow_f32(img, iters, 1.0)
+    assert bad == 0
+    assert_bitexact(got.cpu().numpy(), ref, f"flow iters={iters}")
+
+
+@pytest.mark.parametrize("h,w", [(1, 1), (2, 3), (3, 2), (5, 9), (16, 16), (17, 31), (70, 130)])
+@pytest.mark.parametrize("dt", [1.0, 0.5, 0.3])
+def test_flow_bitexact_small(h, w, dt):
+    img = cf.synth_image(h, w, seed=h + 31 * w, n_rects=2, n_discs=2, sigma=0.2)
+    got = cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(dt=dt, iters=11))
+    ref, _ = oracle.flow_f32(img, 11, dt)
+    assert_bitexact(got.cpu().numpy(), ref, f"flow {h}x{w} dt={dt}")
+
+
+def test_flow_planes():
+    imgs = np.stack([cf.synth_image(60, 150, seed=s, n_rects=3, n_discs=3, sigma=0.08)
+                     for s in range(3)])
+    got = cf.mc_flow(torch.from_numpy(imgs).cuda(), cf.FlowConfig(iters=10)).cpu().numpy()
+    ref, _ = oracle.flow_f32(imgs, 10, 1.0)
+    assert_bitexact(got, ref, "flow planes")
+
+
+def test_flow_u8():
+    q = np.stack([cf.synth_image(54, 96, seed=s, n_rects=3, n_discs=3, sigma=0.1, dtype="u8")
+                  for s in range(4)])
+    for iters in (0, 1, 2, 5, 6):
+        got = cf.mc_flow_u8(torch.from_numpy(q).cuda(), cf.FlowConfig(iters=iters))
+        ref, _ = oracle.flow_f32(oracle.u8_to_f32(q), iters, 1.0)
+        assert_bitexact(got.cpu().numpy(), ref, f"u8 iters={iters}")
+
+
+def test_nonfinite_names_iteration():
+    img = cf.synth_image(40, 70, seed=3, n_rects=2, n_discs=2, sigma=0.1)
+    img[20, 33] = np.nan
+    with pytest.raises(cf.FlowError) as ei:
+        cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(iters=9))
+    assert ei.value.iteration == 1
+    # overflow from finite input: huge values overflow inside the stencil
+    big = np.zeros((16, 16), np.float32)
+    big[8, 8] = 3.0e38
+    _, bad = oracle.flow_f32(big, 5, 1.0)
+    with pytest.raises(cf.FlowError) as ei:
+        cf.mc_flow(torch.from_numpy(big).cuda(), cf.FlowConfig(iters=5))
+    assert ei.value.iteration == bad
+
+
+def test_band_decomposition_bitexact():
+    """Row bands of any size/depth give the single-launch result."""
+    H, W = 203, 300
+    img = cf.synth_image(H, W, seed=11, n_rects=5, n_discs=5, sigma=0.1)
+    ref, _ = oracle.flow_f32(img, 4, 1.0)
+    src = torch.from_numpy(img).cuda()
+    for bands in (1, 2, 3, 7):
+        dst = torch.empty_like(src)
+        edges = [round(i * H / bands) for i in range(bands + 1)]
+        for b in range(bands):
+            cf.sweeps_band(src, 0, dst, 0, H, edges[b], edges[b + 1], 4, 1.0, 0)
+        assert_bitexact(dst.cpu().numpy(), ref, f"bands={bands}")
+
+
+def test_constant_and_impulse():
+    c = np.full((33, 65), 0.3, np.float32)
+    assert np.all(cf.wmc_half_laplace(torch.from_numpy(c).cuda()).cpu().numpy() == 0)
+    f = cf.mc_flow(torch.from_numpy(c).cuda(), cf.FlowConfig(iters=7)).cpu().numpy()
+    assert np.array_equal(f, c)
+    imp = np.zeros((3, 3), np.float32)
+    imp[1, 1] = 1.0
+    m = cf.wmc_half_laplace(torch.from_numpy(imp).cuda()).cpu().numpy()
+    assert m[1, 1] == np.float32(-12.0) * np.float32(1.0 / 12.0)
