@@ -32,7 +32,9 @@ def lib():
             raise RuntimeError(f"{_LIB} missing: run `make -C oracle` (or __graft_entry__.build())")
         L = C.CDLL(_LIB)
         L.or_wmc_map_f64.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp]
-        L.or_wmc_map_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32]
+        L.or_wmc_map_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32, _vp]
+        L.or_wmc_flowmap_f32.argtypes = [_vp, _vp, _i32, _i32, _i32]
+        L.or_wmc_flowmap_f32.restype = C.c_int
         L.or_flow_f32.argtypes = [_vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32, _i32, _pi32]
         L.or_flow_f64.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32, _pi32]
         L.or_u8_to_f32.argtypes = [_vp, _vp, _i64]
@@ -82,16 +84,29 @@ def wmc_naive_f64(img):
     return out
 
 
-def wmc_map_f32(img, threads=None):
-    """fp32 canonical map; img (H, W) or (P, H, W)."""
+def wmc_map_f32(img, threads=None, return_ties=False):
+    """fp32 canonical map with the fp64 near-tie rule; img (H, W) or (P, H, W)."""
     a = np.ascontiguousarray(img, dtype=np.float32)
     a3 = a[None] if a.ndim == 2 else a
     P, h, w = a3.shape
     out = np.empty_like(a3)
+    ties = np.zeros(a3.shape, dtype=np.int8) if return_ties else None
     rc = lib().or_wmc_map_f32(a3.ctypes.data, out.ctypes.data, w, h, w, P, h * w,
-                              _threads(threads))
+                              _threads(threads), ties.ctypes.data if ties is not None else None)
     assert rc == 0
-    return out[0] if a.ndim == 2 else out
+    res = out[0] if a.ndim == 2 else out
+    if return_ties:
+        return res, (ties[0] if a.ndim == 2 else ties)
+    return res
+
+
+def wmc_flowmap_f32(img, threads=None):
+    """H^w as iterated by the flow (canonical fp32, no tie rule)."""
+    a = np.ascontiguousarray(img, dtype=np.float32)
+    h, w = a.shape
+    out = np.empty_like(a)
+    assert lib().or_wmc_flowmap_f32(a.ctypes.data, out.ctypes.data, w, h, _threads(threads)) == 0
+    return out
 
 
 def flow_f32(img, iters, dt=1.0, threads=None):

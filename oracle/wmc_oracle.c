@@ -124,12 +124,16 @@ OR_EXPORT int or_wmc_map_f64(const double* in, double* out, int32_t w, int32_t h
     return 0;
 }
 
-static inline float wmc_at_f32(const float* in, int w, int h, int64_t pitch, int y, int x) {
+static inline float wmc_at_f32(const float* in, int w, int h, int64_t pitch, int y, int x,
+                               int map, int* tie) {
     const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
     const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
     const float* R0 = in + (int64_t)ym * pitch;
     const float* R1 = in + (int64_t)y * pitch;
     const float* R2 = in + (int64_t)yp * pitch;
+    if (map)
+        return wmc_map_px_f32(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x],
+                              R2[xp], tie);
     return wmc_px_f32(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x], R2[xp]);
 }
 
@@ -138,9 +142,10 @@ typedef struct {
     float* out;
     int w, h;
     int64_t pitch;
-    int flow;  /* 0: out = H^w ; 1: out = fmaf(dt, H^w, u) */
+    int flow;  /* 0: map (tie rule) ; 1: out = fmaf(dt, H^w, u) ; 2: flow H^w */
     float dt;
     volatile int* bad; /* per-row non-finite marker (flow only) */
+    int8_t* ties;      /* map only, nullable: 1 where the fp64 tie rule fired */
 } map32_ctx;
 
 static void map32_row(void* vctx, int y) {
@@ -149,8 +154,10 @@ static void map32_row(void* vctx, int y) {
     float* o = c->out + (int64_t)y * c->pitch;
     int bad = 0;
     for (int x = 0; x < c->w; ++x) {
-        float hw = wmc_at_f32(in, c->w, c->h, c->pitch, y, x);
-        if (c->flow) {
+        int tie = 0;
+        float hw = wmc_at_f32(in, c->w, c->h, c->pitch, y, x, !c->flow, &tie);
+        if (c->ties) c->ties[(int64_t)y * c->w + x] = (int8_t)tie;
+        if (c->flow == 1) {
             float v = fmaf(c->dt, hw, in[(int64_t)y * c->pitch + x]);
             if (!isfinite(v)) bad = 1;
             o[x] = v;
@@ -158,17 +165,30 @@ static void map32_row(void* vctx, int y) {
             o[x] = hw;
         }
     }
-    if (c->flow && bad) c->bad[y] = 1;
+    if (c->flow == 1 && bad) c->bad[y] = 1;
 }
 
-/* wmc_half_laplace, fp32 canonical; planes independent. */
+/* wmc_half_laplace, fp32 canonical + fp64 near-tie rule; planes independent
+ * (SPEC.md:62-69).  ties (nullable, planes*h*w) marks pixels resolved in fp64. */
 OR_EXPORT int or_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
-                             int32_t planes, int64_t plane_stride, int32_t threads) {
+                             int32_t planes, int64_t plane_stride, int32_t threads,
+                             int8_t* ties) {
     if (w <= 0 || h <= 0 || planes <= 0 || pitch < w) return 1;
     for (int p = 0; p < planes; ++p) {
-        map32_ctx c = {in + p * plane_stride, out + p * plane_stride, w, h, pitch, 0, 0.f, NULL};
+        map32_ctx c = {in + p * plane_stride, out + p * plane_stride, w, h, pitch, 0, 0.f, NULL,
+                       ties ? ties + (int64_t)p * w * h : NULL};
         for_rows(h, threads, map32_row, &c);
     }
+    return 0;
+}
+
+/* One flow step's H^w field (canonical fp32, no tie rule): the map the flow
+ * iterates, exposed so tests can check U^{t+1} == fmaf(dt, H, U^t). */
+OR_EXPORT int or_wmc_flowmap_f32(const float* in, float* out, int32_t w, int32_t h,
+                                 int32_t threads) {
+    if (w <= 0 || h <= 0) return 1;
+    map32_ctx c = {in, out, w, h, w, 2, 0.f, NULL, NULL};
+    for_rows(h, threads, map32_row, &c);
     return 0;
 }
 
@@ -190,7 +210,7 @@ OR_EXPORT int or_flow_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32
         float* B = tmp;
         for (int t = 1; t <= iters; ++t) {
             memset(bad, 0, sizeof(int) * (size_t)h);
-            map32_ctx c = {A, B, w, h, pitch, 1, dt, bad};
+            map32_ctx c = {A, B, w, h, pitch, 1, dt, bad, NULL};
             for_rows(h, threads, map32_row, &c);
             float* s = A; A = B; B = s;
             int any = 0;

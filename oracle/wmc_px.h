@@ -87,32 +87,79 @@ static inline double wmc_px_f64(const double* in, int w, int h, int64_t pitch, i
 /* ------------------------------------------------------------------------ */
 static const float C12 = 1.0f / 12.0f; /* fl(1/12) = 0x3DAAAAAB */
 
-static inline float wmc_px_f32(float a, float b, float c, float l, float u, float r, float e,
-                               float f, float g) {
+/* first-minimum of |.| as a tournament, left operand wins ties; for finite
+ * inputs identical to the strict-< scan i = 1..8 of SPEC.md:195. */
+static inline float pick_f32(float l, float r) { return fabsf(r) < fabsf(l) ? r : l; }
+
+typedef struct {
+    float D[8];   /* 12 * d_i */
+    float n12u;   /* fl(-12 u) */
+    float best;   /* selected D_m */
+} px32;
+
+static inline void wmc_px_f32_full(float a, float b, float c, float l, float u, float r, float e,
+                                   float f, float g, px32* o) {
     const float n12u = u * -12.0f;
     const float Vl = a + e, Vc = b + f, Vr = c + g;
     const float Wm = Vl + Vc, W0 = Vc + Vr;
     const float Ht = a + c, Hc = l + r, Hb = e + g;
     const float Tm = Ht + Hc, T0 = Hc + Hb;
-    const float D1 = fmaf(2.0f, fmaf(2.0f, l, Wm), n12u);
-    const float D2 = fmaf(2.0f, fmaf(2.0f, b, Tm), n12u);
-    const float D3 = fmaf(2.0f, fmaf(2.0f, r, W0), n12u);
-    const float D4 = fmaf(2.0f, fmaf(2.0f, f, T0), n12u);
+    o->n12u = n12u;
+    o->D[0] = fmaf(2.0f, fmaf(2.0f, l, Wm), n12u);
+    o->D[1] = fmaf(2.0f, fmaf(2.0f, b, Tm), n12u);
+    o->D[2] = fmaf(2.0f, fmaf(2.0f, r, W0), n12u);
+    o->D[3] = fmaf(2.0f, fmaf(2.0f, f, T0), n12u);
     const float K5 = c + e, K6 = a + g;
     const float Pbl = b + l, Pbr = b + r, Prf = r + f, Plf = l + f;
-    const float D5 = fmaf(4.0f, Pbl, fmaf(2.0f, a, K5)) + n12u;
-    const float D6 = fmaf(4.0f, Pbr, fmaf(2.0f, c, K6)) + n12u;
-    const float D7 = fmaf(4.0f, Prf, fmaf(2.0f, g, K5)) + n12u;
-    const float D8 = fmaf(4.0f, Plf, fmaf(2.0f, e, K6)) + n12u;
-    float best = D1;
-    if (fabsf(D2) < fabsf(best)) best = D2;
-    if (fabsf(D3) < fabsf(best)) best = D3;
-    if (fabsf(D4) < fabsf(best)) best = D4;
-    if (fabsf(D5) < fabsf(best)) best = D5;
-    if (fabsf(D6) < fabsf(best)) best = D6;
-    if (fabsf(D7) < fabsf(best)) best = D7;
-    if (fabsf(D8) < fabsf(best)) best = D8;
-    return best * C12;
+    o->D[4] = fmaf(4.0f, Pbl, fmaf(2.0f, a, K5)) + n12u;
+    o->D[5] = fmaf(4.0f, Pbr, fmaf(2.0f, c, K6)) + n12u;
+    o->D[6] = fmaf(4.0f, Prf, fmaf(2.0f, g, K5)) + n12u;
+    o->D[7] = fmaf(4.0f, Plf, fmaf(2.0f, e, K6)) + n12u;
+    const float* D = o->D;
+    o->best = pick_f32(pick_f32(pick_f32(D[0], D[1]), pick_f32(D[2], D[3])),
+                       pick_f32(pick_f32(D[4], D[5]), pick_f32(D[6], D[7])));
 }
 
+/* H^w of the flow: fl(D_m * fl(1/12)). */
+static inline float wmc_px_f32(float a, float b, float c, float l, float u, float r, float e,
+                               float f, float g) {
+    px32 o;
+    wmc_px_f32_full(a, b, c, l, u, r, e, f, g, &o);
+    return o.best * C12;
+}
+
+/* Opposite-sign near-tie test of the map:
+ * T = min_k |fl(D_k + D_m)|, tau = fmaf(|n12u|, 1.5*2^-18, fl(|D_m| * 2^-20)),
+ * tie iff T <= tau && T < |D_m|. */
+static inline int near_tie_f32(const px32* o) {
+    float T = 3.0e38f;
+    for (int k = 0; k < 8; ++k) {
+        float t = fabsf(o->D[k] + o->best);
+        T = t < T ? t : T;
+    }
+    const float tau = fmaf(fabsf(o->n12u), 0x1.8p-19f, fabsf(o->best) * 0x1.0p-20f);
+    return T <= tau && T < fabsf(o->best);
+}
+
+/* The map: canonical fp32, with opposite-sign near-ties resolved by the
+ * SPEC-faithful fp64 evaluation rounded to fp32. */
+static inline float wmc_map_px_f32(float a, float b, float c, float l, float u, float r, float e,
+                                   float f, float g, int* tie) {
+    px32 o;
+    wmc_px_f32_full(a, b, c, l, u, r, e, f, g, &o);
+    if (near_tie_f32(&o)) {
+        pthread_once(&hw_once, init_hw64);
+        const double nb[9] = {a, b, c, l, u, r, e, f, g};
+        double best = 0.0;
+        for (int i = 0; i < 8; ++i) {
+            double s = 0.0;
+            for (int t = 0; t < 9; ++t) s = s + HW64[i][t / 3][t % 3] * nb[t];
+            if (i == 0 || fabs(s) < fabs(best)) best = s;
+        }
+        if (tie) *tie = 1;
+        return (float)best;
+    }
+    if (tie) *tie = 0;
+    return o.best * C12;
+}
 #endif

@@ -21,7 +21,6 @@
 namespace {
 
 constexpr int kMaxLevels = 4;            // sweeps fused per launch
-constexpr int kC = 4;                    // columns per lane
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
 
@@ -61,13 +60,19 @@ int device_info(DevInfo* out) {
     return CF_OK;
 }
 
+template <bool U8>
+constexpr size_t smem_bytes() {
+    return U8 ? 0 : (size_t)cfk::kWarpsPerBlock * cfk::kRingBytesPerWarp;
+}
+
 template <int K, bool MAP, bool VEC, bool U8>
 int kernel_occupancy_warps() {
     static int cached = -1;  // per instantiation; identical on every B200
     if (cached < 0) {
         int blocks = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks, cfk::wmc_sweeps_kernel<kC, K, MAP, VEC, U8>, cfk::kThreads, 0) !=
+                &blocks, cfk::wmc_sweeps_kernel<K, MAP, VEC, U8>, cfk::kThreads,
+                smem_bytes<U8>()) !=
                 cudaSuccess ||
             blocks <= 0)
             blocks = 2;
@@ -80,7 +85,7 @@ int kernel_occupancy_warps() {
 // the per-task length (rows + temporal warm-up + fixed cost) is minimal.
 void plan_strips(cfk::SweepParams& p, int K, int slots) {
     const int rows = p.y1 - p.y0;
-    const int64_t per_strip_tasks = (int64_t)p.n_chunks * p.planes;
+    const int64_t per_strip_tasks = (int64_t)((p.n_chunks + 1) / 2) * p.planes;
     const double overhead = (K - 1) + 6.0;  // warm-up rows + fixed per-task cost (rows)
     const int max_strips = std::max(1, rows / std::max(8, 4 * K));
     double best_cost = 1e300;
@@ -100,13 +105,14 @@ void plan_strips(cfk::SweepParams& p, int K, int slots) {
 
 template <int K, bool MAP, bool VEC, bool U8>
 int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
-    using G = cfk::Geo<kC, K>;
+    using G = cfk::Geo<K>;
     p.n_chunks = (p.w + G::S - 1) / G::S;
     plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MAP, VEC, U8>());
-    const int64_t tasks = (int64_t)p.n_chunks * p.n_strips * p.planes;
+    const int64_t tasks = (int64_t)((p.n_chunks + 1) / 2) * p.n_strips * p.planes;
     const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
     if (blocks > INT_MAX) return CF_EINVAL;
-    cfk::wmc_sweeps_kernel<kC, K, MAP, VEC, U8><<<(unsigned)blocks, cfk::kThreads, 0, s>>>(p);
+    cfk::wmc_sweeps_kernel<K, MAP, VEC, U8>
+        <<<(unsigned)blocks, cfk::kThreads, smem_bytes<U8>(), s>>>(p);
     CF_CUDA(cudaGetLastError());
     return CF_OK;
 }
