@@ -1,0 +1,427 @@
+#!/usr/bin/env python3
+"""Benchmark driver for the B200-native WMC filter.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfg1..cfg5] [--all OUT.json]
+
+Default workload: BASELINE.json configs[3] ("cfg4"), the 16384x16384 fp32
+image filtered for 200 iterations -- the configuration the metric's 1/2/4/8
+GPU scaling is quoted on (row-band sharded across ranks, one process per GPU,
+halo rows exchanged over NCCL each launch).  One STEP = the whole 200-iteration
+filter of that image.  Inputs are seeded synthetic images of the configured
+shape / value distribution; the 1 GiB image exceeds the 126 MB
+L2, so no L2 flush is needed between steps.
+
+Rank 0 prints ONE JSON line (metric, value, e2e, roofline, cpu_baseline,
+clocks, gpu_launches, ...).  ``--impl reference`` times the reference CPU path
+(the fp64 SPEC-faithful restatement in oracle/, all host threads) on a bounded
+sample of the same workload and prints the same line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "WMC Gpixel-updates/s"
+UNIT = "Gpixel-updates/s"
+BYTES_PER_UPDATE = 8  # 4 B read of U^t + 4 B write of U^{t+1}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown", 0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nvml:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------- helpers -----
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_input(cfg, rows=None, threads=0):
+    """Seeded synthetic input (host numpy), all planes; rows = (r0, r1) crop."""
+    import numpy as np
+
+    import paper_1903_07189_b200 as cf
+    imgs = []
+    for p in range(cfg.planes):
+        a = cf.synth_image(cfg.h, cfg.w, cfg.seed(p), cfg.n_rects, cfg.n_discs, cfg.sigma,
+                           dtype="u8" if cfg.u8 else "f32", threads=threads)
+        imgs.append(a if rows is None else a[rows[0]:rows[1]])
+    return np.stack(imgs) if cfg.planes > 1 else imgs[0]
+
+
+def cpu_reference_sample(cfg, full, target_s=8.0):
+    """Time the reference CPU path (fp64 SPEC-faithful mc_flow / map, all host
+    threads) on a bounded crop of the workload's input `full` (plane 0).
+    Returns (Gupd/s, cores, sample description, kind)."""
+    import numpy as np
+
+    import oracle
+    threads = os.cpu_count() or 1
+    crop_h = min(cfg.h, 2048)
+    crop_w = min(cfg.w, 2048)
+    img = np.ascontiguousarray(full[:crop_h, :crop_w], dtype=np.float64)
+    if cfg.u8:
+        img = img / 255.0
+    if cfg.iters == 0:
+        fn = lambda n: [oracle.wmc_map_f64(img, threads) for _ in range(n)]  # noqa: E731
+    else:
+        fn = lambda n: oracle.flow_f64(img, n, cfg.dt, threads)  # noqa: E731
+    fn(1)  # warm (page-in, thread spawn)
+    t0 = time.perf_counter()
+    fn(1)
+    per = max(time.perf_counter() - t0, 1e-6)
+    n = max(1, min(cfg.iters if cfg.iters else 50, int(target_s / per)))
+    t0 = time.perf_counter()
+    fn(n)
+    dt = time.perf_counter() - t0
+    rate = crop_h * crop_w * n / dt / 1e9
+    sample = (f"fp64 SPEC-faithful {'mc_flow' if cfg.iters else 'wmc_half_laplace'} "
+              f"(oracle/wmc_oracle.c, for_rows restatement) on a {crop_h}x{crop_w} crop of "
+              f"the {cfg.name} input, {n} iteration(s), {dt:.1f} s")
+    return rate, threads, sample, "port"
+
+
+# ------------------------------------------------------------- b200 arm ----
+def bench_b200(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1903_07189_b200 as cf
+    from paper_1903_07189_b200 import sharded
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = cf.lib()
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    # ---------------- inputs (host, pinned) and device buffers ----------------
+    K = 2  # sweeps per launch, = the C-ABI filter's schedule
+    if world > 1 and cfg.sharding == "rows":
+        lay = sharded.BandLayout(cfg.h, cfg.w, rank, world, K)
+        rows = (lay.r0, lay.r1)
+    elif world > 1 and cfg.sharding == "images":
+        per = (cfg.planes + world - 1) // world
+        p0, p1 = rank * per, min(cfg.planes, (rank + 1) * per)
+        rows = None
+    else:
+        rows = None
+    host = make_input(cfg, rows=rows)
+    if world > 1 and cfg.sharding == "images":
+        host = host[p0:p1]
+    host_t = torch.from_numpy(np.ascontiguousarray(host)).pin_memory()
+    out_host = torch.empty(host_t.shape, dtype=torch.float32).pin_memory()
+    dev_in = host_t.to(dev)
+    n_px_local = int(np.prod(host.shape))
+    P, H, W = (host.shape if host.ndim == 3 else (1,) + host.shape)
+    updates_local = n_px_local * max(1, cfg.iters)
+    launches_per_step = 0
+
+    if cfg.iters == 0:  # single map evaluation (cfg1)
+        out = torch.empty(dev_in.shape, dtype=torch.float32, device=dev)
+
+        def step():
+            cf.lib().cf_wmc_map_f32(dev_in.data_ptr(), out.data_ptr(), W, H, W, P, H * W, sp)
+        launches_per_step = 1
+    elif world > 1 and cfg.sharding == "rows":
+        buf_a = torch.zeros((lay.rows, cfg.w), dtype=torch.float32, device=dev)
+        buf_b = torch.zeros_like(buf_a)
+        flag = torch.full((1,), 0x7F7F7F7F, dtype=torch.int32, device=dev)
+        flow = sharded.ShardedFlow(lay, sharded.cuda_compute(flag), dist)
+
+        def step():
+            buf_a[lay.band_slice()].copy_(dev_in)
+            res = flow.run(buf_a, buf_b, cfg.iters, cfg.dt)
+            return res
+        launches_per_step = len(sharded.launch_schedule(cfg.iters, K))
+    else:
+        work = torch.empty(dev_in.shape, dtype=torch.float32, device=dev)
+        nbytes = int(L.cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        import ctypes
+        bad = ctypes.c_int32(0)
+        if cfg.u8:
+            def step():
+                rc = L.cf_wmc_filter_u8_f32(dev_in.data_ptr(), W, H * W, work.data_ptr(), W, H,
+                                            W, P, H * W, cfg.iters, cfg.dt, ws.data_ptr(),
+                                            nbytes, ctypes.byref(bad), sp)
+                assert rc == 0, rc
+        else:
+            def step():
+                work.copy_(dev_in)  # the filter is in place; restore U^0 each step
+                rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, cfg.iters, cfg.dt,
+                                         ws.data_ptr(), nbytes, ctypes.byref(bad), sp)
+                assert rc == 0, rc
+        launches_per_step = int(L.cf_wmc_filter_launches(cfg.iters))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, steps):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / steps
+
+    # ---------------- device-resident timing (value) ----------------
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(local) as clk:
+        ms_step = timed(step, args.steps)
+    updates_job = cfg.updates  # whole job over all ranks (strong scaling for rows)
+    if world > 1 and cfg.sharding == "images":
+        updates_job = updates_local * world  # per-rank fixed share (weak scaling)
+    value = updates_job / (ms_step * 1e-3) / 1e9
+
+    # ---------------- dominant kernel: average launch duration ----------------
+    kern_ms = None
+    if cfg.iters > 0 and not (world > 1):
+        src = torch.empty((H, W), dtype=torch.float32, device=dev).copy_(
+            dev_in[0] if P > 1 else dev_in) if not cfg.u8 else torch.rand((H, W), device=dev)
+        dst = torch.empty_like(src)
+        reps = 20
+        for _ in range(3):
+            cf.sweeps_band(src, 0, dst, 0, H, 0, H, K, cfg.dt, 0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for i in range(reps):
+            cf.sweeps_band(src if i % 2 == 0 else dst, 0, dst if i % 2 == 0 else src, 0, H, 0, H,
+                           K, cfg.dt, 0)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        kern_ms = e0.elapsed_time(e1) / reps
+        kern_updates = H * W * K
+    elif cfg.iters == 0:
+        kern_ms, kern_updates = ms_step, n_px_local
+    peak, peak_src = peaks()
+
+    # ---------------- end-to-end through the public API, host buffers ----------
+    def e2e_step():
+        d_in = host_t.to(dev, non_blocking=True)
+        if cfg.iters == 0:
+            r = cf.wmc_half_laplace(d_in)
+        elif world > 1 and cfg.sharding == "rows":
+            buf_a[lay.band_slice()].copy_(d_in)
+            r = flow.run(buf_a, buf_b, cfg.iters, cfg.dt)[lay.band_slice()]
+        elif cfg.u8:
+            r = cf.mc_flow_u8(d_in, cf.FlowConfig(dt=cfg.dt, iters=cfg.iters), workspace=ws)
+        else:
+            r = cf.mc_flow(d_in, cf.FlowConfig(dt=cfg.dt, iters=cfg.iters), workspace=ws,
+                           inplace=True)
+        out_host.copy_(r.reshape(out_host.shape), non_blocking=True)
+    e2e_steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        e2e_step()
+    ms_e2e = timed(e2e_step, e2e_steps)
+    e2e_value = updates_job / (ms_e2e * 1e-3) / 1e9
+    h2d = host_t.numel() * host_t.element_size()
+    d2h = out_host.numel() * out_host.element_size()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    res = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak" if cfg.sharding == "images" else "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator, DESIGN.md §6)",
+        "config": {
+            "workload": f"{cfg.name}: {cfg.planes}x{cfg.h}x{cfg.w} "
+                        f"{'u8' if cfg.u8 else 'f32'}, {cfg.iters or 1} "
+                        f"{'iterations' if cfg.iters else 'map evaluation'}, dt={cfg.dt}",
+            "iters": cfg.iters, "planes": cfg.planes, "h": cfg.h, "w": cfg.w,
+            "sweeps_per_launch": 1 if cfg.iters == 0 else K,
+            "parallelism": (f"rowband{world}" if cfg.sharding == "rows" and world > 1 else
+                            f"images{world}" if world > 1 else "single"),
+            "l2": "inputs larger than L2 (126 MB)" if n_px_local * 4 > 126e6 else
+                  "L2-resident working set (no flush; flagged)",
+        },
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if kern_ms is not None:
+        achieved = kern_updates * BYTES_PER_UPDATE / (kern_ms * 1e-3) / 1e9
+        res["roofline"] = {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "wmc_sweeps_kernel<K=2>" if cfg.iters else "wmc_sweeps_kernel<MAP>",
+            "kernel_ms": round(kern_ms, 4), "peak_source": peak_src,
+            "note": "algorithmic 8 B per pixel-update x updates per launch / launch time; "
+                    "physical DRAM bytes per launch are in profiles/ (ncu)",
+        }
+    if world == 1 and not args.no_cpu_baseline:
+        rate, cores, sample, kind = cpu_reference_sample(cfg, host[0] if host.ndim == 3 else host)
+        res["cpu_baseline"] = {"value": round(rate, 4), "unit": UNIT, "cores": cores,
+                               "kind": kind, "sample": sample}
+    if world > 1:
+        dist.destroy_process_group()
+    return res
+
+
+# -------------------------------------------------------- reference arm ----
+def bench_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    import numpy as np
+
+    import oracle
+    threads = os.cpu_count() or 1
+    crop = min(cfg.h, 2048), min(cfg.w, 2048)
+    full = make_input(cfg.__class__(**{**cfg.__dict__, "planes": 1}))
+    img = np.ascontiguousarray(full[:crop[0], :crop[1]], dtype=np.float64)
+    if cfg.u8:
+        img = img / 255.0
+    n_it = 1 if cfg.iters == 0 else 2
+
+    def sample():
+        if cfg.iters == 0:
+            oracle.wmc_map_f64(img, threads)
+        else:
+            oracle.flow_f64(img, n_it, cfg.dt, threads)
+    for _ in range(args.warmup):
+        sample()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sample()
+    dt = time.perf_counter() - t0
+    rate = crop[0] * crop[1] * n_it * args.steps / dt / 1e9
+    desc = (f"fp64 SPEC-faithful {'wmc_half_laplace' if cfg.iters == 0 else 'mc_flow'} "
+            f"(oracle/wmc_oracle.c, the reference algorithm restated; for_rows executor) on a "
+            f"{crop[0]}x{crop[1]} crop of the {cfg.name} input, {n_it} iteration(s) per step")
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(rate, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak" if cfg.sharding == "images" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator, DESIGN.md §6)",
+        "config": {"workload": f"{cfg.name} (bounded CPU sample)", "iters": cfg.iters,
+                   "planes": cfg.planes, "h": cfg.h, "w": cfg.w},
+        "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": threads,
+                         "kind": "port", "sample": desc},
+        "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--all", default=None, help="run every config at N=1, write JSON lines")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    from paper_1903_07189_b200.configs import CONFIGS
+    if args.all:
+        with open(args.all, "w") as f:
+            for name in CONFIGS:
+                r = bench_b200(args, CONFIGS[name])
+                if r:
+                    f.write(json.dumps(r) + "\n")
+                    f.flush()
+                    print(json.dumps(r), flush=True)
+        return
+    cfg = CONFIGS[args.workload]
+    res = bench_reference(args, cfg) if args.impl == "reference" else bench_b200(args, cfg)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,8 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
 /* atomically min-ed with the first iteration producing a non-finite value.*/
 /* ---------------------------------------------------------------------- */
 CF_API int32_t cf_wmc_max_sweeps_per_launch(void);
+/* Number of kernel launches cf_wmc_filter_f32 / _u8_f32 enqueue for iters. */
+CF_API int32_t cf_wmc_filter_launches(int32_t iters);
 CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,
                                   float* dst, int32_t dst_row0, int32_t w, int32_t h,
                                   int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,

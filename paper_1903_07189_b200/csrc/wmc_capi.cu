@@ -20,7 +20,9 @@
 
 namespace {
 
-constexpr int kMaxLevels = 4;            // sweeps fused per launch
+constexpr int kMaxLevels = 4;            // max sweeps fused per launch (band API)
+constexpr int kFlowLevels = 2;           // sweeps per launch the filter schedules (measured
+                                         // fastest on B200, DESIGN.md §4 / profiles/)
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
 
@@ -141,13 +143,13 @@ bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane
     return true;
 }
 
-// Launch schedule: sweeps per launch, at most kMaxLevels each, an EVEN number
+// Launch schedule: sweeps per launch, at most kFlowLevels each, an EVEN number
 // of launches when iters >= 2 so the ping-pong ends in the caller's buffer.
 std::vector<int> schedule(int iters) {
     std::vector<int> ks;
     int left = iters;
     while (left > 0) {
-        const int k = std::min(left, kMaxLevels);
+        const int k = std::min(left, kFlowLevels);
         ks.push_back(k);
         left -= k;
     }
@@ -155,8 +157,10 @@ std::vector<int> schedule(int iters) {
         // split the largest launch (>= 2 sweeps) into two
         auto it = std::max_element(ks.begin(), ks.end());
         const int k = *it;
-        *it = k / 2;
-        ks.insert(it + 1, k - k / 2);
+        if (k >= 2) {
+            *it = k / 2;
+            ks.insert(it + 1, k - k / 2);
+        }
     }
     return ks;
 }
@@ -193,6 +197,11 @@ CF_API const char* cf_status_string(int status) {
 CF_API int cf_last_cuda_error(void) { return g_last_cuda; }
 
 CF_API int32_t cf_wmc_max_sweeps_per_launch(void) { return kMaxLevels; }
+
+CF_API int32_t cf_wmc_filter_launches(int32_t iters) {
+    if (iters <= 0) return 0;
+    return (int32_t)schedule(iters).size();
+}
 
 CF_API void cf_kernel_bank_x12(int32_t* out72) {
     // PAPER.md:411-444; SPEC.md:96-111 -- h_i * 12, [i][row][col]

@@ -1,0 +1,114 @@
+"""Row-band sharded WMC flow across ranks (BASELINE cfg 4: one huge image).
+
+One process per GPU.  The image's rows are split like the reference's
+``curveflow::parallel::for_rows`` (contiguous ceil-div blocks,
+proj/include/curveflow/parallel.hpp:36-44); each rank owns one band and keeps
+``k`` halo rows above and below it.  Before every launch of ``kk <= k`` fused
+sweeps the ranks exchange the ``kk`` boundary rows of the current iterate with
+their neighbours (point-to-point over NCCL / NVLink; gloo in the CPU tests),
+then each rank advances its band ``kk`` iterations with the row-band kernel
+(C-ABI ``cf_wmc_sweeps_band_f32``).  Jacobi semantics make the result
+bit-identical to the single-GPU filter for any band count.
+
+The compute step is injected, so the exchange protocol is the same code in
+the GPU bench (CUDA kernel) and in the CPU tests (oracle compute over gloo).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Tuple
+
+
+def band_bounds(h: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous ceil-div row blocks (parallel.hpp:36-44); one per rank."""
+    if world < 1 or h < world:
+        raise ValueError(f"cannot split {h} rows over {world} ranks")
+    chunk = (h + world - 1) // world
+    bands = []
+    for p in range(world):
+        r0, r1 = min(h, p * chunk), min(h, (p + 1) * chunk)
+        if r0 >= r1:
+            raise ValueError(f"rank {p} would own no rows (h={h}, world={world})")
+        bands.append((r0, r1))
+    return bands
+
+
+def launch_schedule(iters: int, k: int) -> List[int]:
+    """Sweeps per launch: chunks of k, remainder last."""
+    ks, left = [], iters
+    while left > 0:
+        ks.append(min(k, left))
+        left -= ks[-1]
+    return ks
+
+
+# compute(src, src_row0, dst, dst_row0, h, y0, y1, sweeps, dt, iter_base)
+ComputeFn = Callable[..., None]
+
+
+@dataclass
+class BandLayout:
+    h: int
+    w: int
+    rank: int
+    world: int
+    k: int
+
+    def __post_init__(self):
+        self.r0, self.r1 = band_bounds(self.h, self.world)[self.rank]
+        if self.r1 - self.r0 < self.k and self.world > 1:
+            raise ValueError("band height must be >= sweeps per launch")
+        self.top = self.k if self.rank > 0 else 0
+        self.bot = self.k if self.rank < self.world - 1 else 0
+        self.rows = self.top + (self.r1 - self.r0) + self.bot
+        self.buf_row0 = self.r0 - self.top  # global row of buffer row 0
+
+    def band_slice(self):
+        return slice(self.top, self.top + self.r1 - self.r0)
+
+
+class ShardedFlow:
+    """Sharded mc_flow over a band buffer pair (torch tensors, any device)."""
+
+    def __init__(self, layout: BandLayout, compute: ComputeFn, dist, group=None):
+        self.L = layout
+        self.compute = compute
+        self.dist = dist
+        self.group = group
+
+    def exchange(self, buf, kk: int) -> None:
+        """Fill the kk halo rows nearest the band from the neighbours' bands."""
+        L, dist = self.L, self.dist
+        ops = []
+        b0, b1 = L.top, L.top + (L.r1 - L.r0)
+        if L.rank > 0:
+            ops.append(dist.P2POp(dist.isend, buf[b0:b0 + kk], L.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf[b0 - kk:b0], L.rank - 1, self.group))
+        if L.rank < L.world - 1:
+            ops.append(dist.P2POp(dist.isend, buf[b1 - kk:b1], L.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf[b1:b1 + kk], L.rank + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def run(self, buf_a, buf_b, iters: int, dt: float):
+        """buf_a holds U^0 in its band rows; returns the buffer holding U^iters."""
+        L = self.L
+        cur, nxt = buf_a, buf_b
+        it = 0
+        for kk in launch_schedule(iters, L.k):
+            self.exchange(cur, kk)
+            # src covers [max(0, r0-kk), min(h, r1+kk)); dst rows [r0, r1)
+            self.compute(cur, L.buf_row0, nxt, L.buf_row0, L.h, L.r0, L.r1, kk, dt, it)
+            it += kk
+            cur, nxt = nxt, cur
+        return cur
+
+
+def cuda_compute(flag=None) -> ComputeFn:
+    """Row-band kernel through the C-ABI (cf_wmc_sweeps_band_f32)."""
+    from .curveflow import sweeps_band
+
+    def fn(src, src_row0, dst, dst_row0, h, y0, y1, sweeps, dt, iter_base):
+        sweeps_band(src, src_row0, dst, dst_row0, h, y0, y1, sweeps, dt, iter_base, flag)
+    return fn
