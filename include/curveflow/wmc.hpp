@@ -1,0 +1,146 @@
+// include/curveflow/wmc.hpp -- C++ host API of the B200 WMC path.
+//
+// Mirrors the reference's C++ surface in namespace curveflow (SPEC.md:29-89
+// core types, :250-253 FlowConfig, :171 wmc_half_laplace, :256 mc_flow;
+// the reference's only shipped header is curveflow/parallel.hpp) on top of
+// the C-ABI in capi.h.  Header-only; link libcurveflow_b200.so and cudart.
+//
+//   curveflow::Image2D img = ...;                         // host, row-major
+//   auto hw  = curveflow::cuda::wmc_half_laplace(img);     // H2D, kernel, D2H
+//   auto out = curveflow::cuda::mc_flow(img, {1.0, 100});  // throws FlowError
+//
+// Device-pointer overloads (curveflow::cuda::device::...) skip the copies and
+// are stream-ordered.  There is no CPU fallback.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "capi.h"
+
+namespace curveflow {
+
+// SPEC.md:34-39.  This build computes in fp32; data.size()
+// == width * height, row-major, x = column, y = row.
+struct Image2D {
+    int width = 0, height = 0;
+    std::vector<float> data;
+    Image2D() = default;
+    Image2D(int w, int h, float v = 0.0f) : width(w), height(h), data((size_t)w * h, v) {}
+    float& at(int y, int x) { return data[(size_t)y * width + x]; }
+    float at(int y, int x) const { return data[(size_t)y * width + x]; }
+};
+
+// SPEC.md:250-253.  dt default 1.0 for half_laplace; 0 < dt <= 1.
+struct FlowConfig {
+    double dt = 1.0;
+    int iters = 0;
+    enum class Scheme { half_laplace, fd } scheme = Scheme::half_laplace;
+};
+
+class Error : public std::runtime_error {
+   public:
+    Error(int status, const std::string& what)
+        : std::runtime_error(what + ": " + cf_status_string(status)), status_(status) {}
+    int status() const { return status_; }
+
+   private:
+    int status_;
+};
+
+// mc_flow aborts naming the iteration that went non-finite.
+class FlowError : public Error {
+   public:
+    explicit FlowError(int iteration)
+        : Error(CF_ENONFINITE, "mc_flow: non-finite value at iteration " +
+                                   std::to_string(iteration)),
+          iteration_(iteration) {}
+    int iteration() const { return iteration_; }
+
+   private:
+    int iteration_;
+};
+
+namespace detail {
+inline void check(int st, const char* what) {
+    if (st != CF_OK) throw Error(st, what);
+}
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t n) { cuda_check(cudaMalloc(&p, n ? n : 1), "cudaMalloc"); }
+    ~DevBuf() { cudaFree(p); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+}  // namespace detail
+
+namespace cuda {
+
+// Device-pointer entry points (stream-ordered; pointers owned by the caller).
+namespace device {
+inline void wmc_half_laplace(const float* in, float* out, int w, int h, cudaStream_t s = nullptr) {
+    detail::check(cf_wmc_map_f32(in, out, w, h, w, 1, (int64_t)w * h, s), "wmc_half_laplace");
+}
+inline void mc_flow(float* img, int w, int h, const FlowConfig& cfg, void* workspace,
+                    size_t workspace_bytes, cudaStream_t s = nullptr) {
+    if (cfg.scheme != FlowConfig::Scheme::half_laplace)
+        throw std::invalid_argument("scheme=fd is outside this build (DESIGN.md §9)");
+    int32_t bad = 0;
+    const int st = cf_wmc_filter_f32(img, w, h, w, 1, (int64_t)w * h, cfg.iters, (float)cfg.dt,
+                                     workspace, workspace_bytes, &bad, s);
+    if (st == CF_ENONFINITE) throw FlowError(bad);
+    detail::check(st, "mc_flow");
+}
+inline size_t flow_workspace_bytes(int w, int h) {
+    return cf_wmc_filter_workspace_bytes(w, h, w, 1, (int64_t)w * h);
+}
+}  // namespace device
+
+// wmc_half_laplace(img) -> Image2D, host in / host out.
+inline Image2D wmc_half_laplace(const Image2D& img, cudaStream_t s = nullptr) {
+    Image2D out(img.width, img.height);
+    const size_t n = img.data.size() * sizeof(float);
+    detail::DevBuf din(n), dout(n);
+    detail::cuda_check(cudaMemcpyAsync(din.p, img.data.data(), n, cudaMemcpyHostToDevice, s),
+                       "H2D");
+    device::wmc_half_laplace((const float*)din.p, (float*)dout.p, img.width, img.height, s);
+    detail::cuda_check(cudaMemcpyAsync(out.data.data(), dout.p, n, cudaMemcpyDeviceToHost, s),
+                       "D2H");
+    detail::cuda_check(cudaStreamSynchronize(s), "sync");
+    return out;
+}
+
+// mc_flow(img, cfg) -> Image2D (scheme = half_laplace).
+inline Image2D mc_flow(const Image2D& img, const FlowConfig& cfg, cudaStream_t s = nullptr) {
+    Image2D out = img;
+    if (cfg.iters == 0) return out;
+    const size_t n = img.data.size() * sizeof(float);
+    detail::DevBuf dimg(n), ws(device::flow_workspace_bytes(img.width, img.height));
+    detail::cuda_check(cudaMemcpyAsync(dimg.p, img.data.data(), n, cudaMemcpyHostToDevice, s),
+                       "H2D");
+    device::mc_flow((float*)dimg.p, img.width, img.height, cfg, ws.p,
+                    device::flow_workspace_bytes(img.width, img.height), s);
+    detail::cuda_check(cudaMemcpyAsync(out.data.data(), dimg.p, n, cudaMemcpyDeviceToHost, s),
+                       "D2H");
+    detail::cuda_check(cudaStreamSynchronize(s), "sync");
+    return out;
+}
+
+// Per-channel processing: planes are independent.
+inline std::vector<Image2D> mc_flow(const std::vector<Image2D>& channels, const FlowConfig& cfg) {
+    if (channels.size() != 1 && channels.size() != 3)
+        throw std::invalid_argument("unsupported channel count (SPEC.md:65)");
+    std::vector<Image2D> out;
+    for (const auto& c : channels) out.push_back(mc_flow(c, cfg));
+    return out;
+}
+
+}  // namespace cuda
+}  // namespace curveflow

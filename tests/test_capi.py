@@ -126,3 +126,10 @@ def test_product_has_no_oracle_dependency():
                     for line in open(path):
                         if line.lstrip().startswith("#include") or f == "Makefile":
                             assert "oracle" not in line, (f, line)
+
+
+def test_cpp_cli_built():
+    exe = os.path.join(os.path.dirname(_lib.LIB_PATH), "curveflow_b200")
+    assert os.access(exe, os.X_OK)
+    r = __import__("subprocess").run([exe], capture_output=True, text=True)
+    assert r.returncode == 2 and "usage" in r.stderr

@@ -129,3 +129,27 @@ def test_constant_and_impulse():
     imp[1, 1] = 1.0
     m = cf.wmc_half_laplace(torch.from_numpy(imp).cuda()).cpu().numpy()
     assert m[1, 1] == np.float32(-12.0) * np.float32(1.0 / 12.0)
+
+
+def test_cpp_cli_matches_oracle():
+    """C++ host code -> C++ API (include/curveflow/wmc.hpp) -> C-ABI -> kernels."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(cf.LIB_PATH), "curveflow_b200")
+    H, W, it = 45, 77, 9
+    img = cf.synth_image(H, W, seed=3, n_rects=20, n_discs=20, sigma=0.1)
+
+    def fnv(a):
+        h = 1469598103934665603
+        for byte in np.ascontiguousarray(a, np.float32).tobytes():
+            h = ((h ^ byte) * 1099511628211) & (2**64 - 1)
+        return f"{h:016x}"
+    out = json.loads(subprocess.run([exe, "flow", "--size", str(H), str(W), "--seed", "3",
+                                     "--iters", str(it)], capture_output=True, text=True,
+                                    check=True).stdout)
+    ref, _ = oracle.flow_f32(img, it, 1.0)
+    assert out["fnv1a"] == fnv(ref)
+    out = json.loads(subprocess.run([exe, "op", "--size", str(H), str(W), "--seed", "3"],
+                                    capture_output=True, text=True, check=True).stdout)
+    assert out["fnv1a"] == fnv(oracle.wmc_map_f32(img))
