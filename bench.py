@@ -169,7 +169,7 @@ def bench_b200(args, cfg):
     sp = stream.cuda_stream
 
     # ---------------- inputs (host, pinned) and device buffers ----------------
-    K = 2  # sweeps per launch, = the C-ABI filter's schedule
+    K = 3  # sweeps per launch, = the C-ABI filter's schedule
     if world > 1 and cfg.sharding == "rows":
         lay = sharded.BandLayout(cfg.h, cfg.w, rank, world, K)
         rows = (lay.r0, lay.r1)
@@ -335,7 +335,7 @@ def bench_b200(args, cfg):
         res["roofline"] = {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "wmc_sweeps_kernel<K=2>" if cfg.iters else "wmc_sweeps_kernel<MAP>",
+            "kernel": f"wmc_sweeps_kernel<K={K}>" if cfg.iters else "wmc_sweeps_kernel<MAP>",
             "kernel_ms": round(kern_ms, 4), "peak_source": peak_src,
             "note": "algorithmic 8 B per pixel-update x updates per launch / launch time; "
                     "physical DRAM bytes per launch are in profiles/ (ncu)",

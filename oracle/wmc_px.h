@@ -75,14 +75,15 @@ static inline double wmc_px_f64(const double* in, int w, int h, int64_t pitch, i
 /*   l u r        12*d2 = 2((a+c)+(l+r)) + 4b - 12u       (h2)               */
 /*   e f g        12*d3 = 2((b+f)+(c+g)) + 4r - 12u       (h3)               */
 /*                12*d4 = 2((l+r)+(e+g)) + 4f - 12u       (h4)               */
-/*                12*d5 = 4(b+l) + 2a + (c+e) - 12u       (h5)               */
-/*                12*d6 = 4(b+r) + 2c + (a+g) - 12u       (h6)               */
-/*                12*d7 = 4(r+f) + 2g + (c+e) - 12u       (h7)               */
-/*                12*d8 = 4(l+f) + 2e + (a+g) - 12u       (h8)               */
+/*                12*d5 = 4(b+l) + 2a + ((c+e) - 12u)     (h5)               */
+/*                12*d6 = 4(b+r) + 2c + ((a+g) - 12u)     (h6)               */
+/*                12*d7 = 4(r+f) + 2g + ((c+e) - 12u)     (h7)               */
+/*                12*d8 = 4(l+f) + 2e + ((a+g) - 12u)     (h8)               */
 /*                                                                           */
 /* ×2 and ×4 are exact, so fmaf(2,x,y) is the single rounding of 2x+y.       */
-/* n12u = fl(u * -12) is formed once and ADDED, so a constant image gives    */
-/* exact zeros (fl(2*fl(6u)) == fl(12u)).  D_m selected by strict < on |D|   */
+/* n12u = fl(u * -12) is formed once and ADDED; D1..D4 of a constant image   */
+/* are exact zeros (fl(2*fl(6u)) == fl(12u)) and D1 wins the selection, so   */
+/* the map / flow of a constant is exact.  D_m selected by strict < on |D|   */
 /* scanning 1..8; H^w = fl(D_m * fl(1/12)); flow step fmaf(dt, H^w, u).       */
 /* ------------------------------------------------------------------------ */
 static const float C12 = 1.0f / 12.0f; /* fl(1/12) = 0x3DAAAAAB */
@@ -109,12 +110,12 @@ static inline void wmc_px_f32_full(float a, float b, float c, float l, float u, 
     o->D[1] = fmaf(2.0f, fmaf(2.0f, b, Tm), n12u);
     o->D[2] = fmaf(2.0f, fmaf(2.0f, r, W0), n12u);
     o->D[3] = fmaf(2.0f, fmaf(2.0f, f, T0), n12u);
-    const float K5 = c + e, K6 = a + g;
+    const float K5 = (c + e) + n12u, K6 = (a + g) + n12u;
     const float Pbl = b + l, Pbr = b + r, Prf = r + f, Plf = l + f;
-    o->D[4] = fmaf(4.0f, Pbl, fmaf(2.0f, a, K5)) + n12u;
-    o->D[5] = fmaf(4.0f, Pbr, fmaf(2.0f, c, K6)) + n12u;
-    o->D[6] = fmaf(4.0f, Prf, fmaf(2.0f, g, K5)) + n12u;
-    o->D[7] = fmaf(4.0f, Plf, fmaf(2.0f, e, K6)) + n12u;
+    o->D[4] = fmaf(4.0f, Pbl, fmaf(2.0f, a, K5));
+    o->D[5] = fmaf(4.0f, Pbr, fmaf(2.0f, c, K6));
+    o->D[6] = fmaf(4.0f, Prf, fmaf(2.0f, g, K5));
+    o->D[7] = fmaf(4.0f, Plf, fmaf(2.0f, e, K6));
     const float* D = o->D;
     o->best = pick_f32(pick_f32(pick_f32(D[0], D[1]), pick_f32(D[2], D[3])),
                        pick_f32(pick_f32(D[4], D[5]), pick_f32(D[6], D[7])));

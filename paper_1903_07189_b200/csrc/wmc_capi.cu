@@ -21,7 +21,7 @@
 namespace {
 
 constexpr int kMaxLevels = 4;            // max sweeps fused per launch (band API)
-constexpr int kFlowLevels = 2;           // sweeps per launch the filter schedules (measured
+constexpr int kFlowLevels = 3;           // sweeps per launch the filter schedules (measured
                                          // fastest on B200, DESIGN.md §4 / profiles/)
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
@@ -62,19 +62,22 @@ int device_info(DevInfo* out) {
     return CF_OK;
 }
 
-template <bool U8>
+template <int K>
 constexpr size_t smem_bytes() {
-    return U8 ? 0 : (size_t)cfk::kWarpsPerBlock * cfk::kRingBytesPerWarp;
+    return (size_t)cfk::kWarpsPerBlock * cfk::smem_bytes_per_warp<K>();
 }
 
-template <int K, bool MAP, bool VEC, bool U8>
+template <int K, bool MAP>
 int kernel_occupancy_warps() {
     static int cached = -1;  // per instantiation; identical on every B200
     if (cached < 0) {
+        if (smem_bytes<K>() > 48 * 1024)
+            cudaFuncSetAttribute(cfk::wmc_sweeps_kernel<K, MAP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<K>());
         int blocks = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks, cfk::wmc_sweeps_kernel<K, MAP, VEC, U8>, cfk::kThreads,
-                smem_bytes<U8>()) !=
+                &blocks, cfk::wmc_sweeps_kernel<K, MAP>, cfk::kThreads,
+                smem_bytes<K>()) !=
                 cudaSuccess ||
             blocks <= 0)
             blocks = 2;
@@ -105,36 +108,34 @@ void plan_strips(cfk::SweepParams& p, int K, int slots) {
     p.n_strips = (rows + p.strip_rows - 1) / p.strip_rows;
 }
 
-template <int K, bool MAP, bool VEC, bool U8>
+template <int K, bool MAP>
 int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
     using G = cfk::Geo<K>;
     p.n_chunks = (p.w + G::S - 1) / G::S;
-    plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MAP, VEC, U8>());
+    plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MAP>());
     const int64_t tasks = (int64_t)((p.n_chunks + 1) / 2) * p.n_strips * p.planes;
     const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
     if (blocks > INT_MAX) return CF_EINVAL;
-    cfk::wmc_sweeps_kernel<K, MAP, VEC, U8>
-        <<<(unsigned)blocks, cfk::kThreads, smem_bytes<U8>(), s>>>(p);
+    cfk::wmc_sweeps_kernel<K, MAP><<<(unsigned)blocks, cfk::kThreads, smem_bytes<K>(), s>>>(p);
     CF_CUDA(cudaGetLastError());
     return CF_OK;
 }
 
-template <bool MAP, bool VEC, bool U8>
+template <bool MAP>
 int launch(const cfk::SweepParams& p, int K, const DevInfo& d, cudaStream_t s) {
     if constexpr (MAP) {
-        return launch_k<1, true, VEC, U8>(p, d, s);
+        return launch_k<1, true>(p, d, s);
     } else {
         switch (K) {
-            case 1: return launch_k<1, false, VEC, U8>(p, d, s);
-            case 2: return launch_k<2, false, VEC, U8>(p, d, s);
-            case 3: return launch_k<3, false, VEC, U8>(p, d, s);
-            case 4: return launch_k<4, false, VEC, U8>(p, d, s);
+            case 1: return launch_k<1, false>(p, d, s);
+            case 2: return launch_k<2, false>(p, d, s);
+            case 3: return launch_k<3, false>(p, d, s);
+            case 4: return launch_k<4, false>(p, d, s);
             default: return CF_EINVAL;
         }
     }
 }
 
-bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
 
 bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane_stride) {
     if (w <= 0 || h <= 0 || planes <= 0 || pitch < w) return false;
@@ -230,10 +231,7 @@ CF_API int cf_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int
     p.src_row0 = p.dst_row0 = 0;
     p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
     p.dt = 0.f; p.iter_base = 0; p.flag = nullptr;
-    const bool vec = pitch % 4 == 0 && (planes == 1 || plane_stride % 4 == 0) && aligned16(in) &&
-                     aligned16(out);
-    cudaStream_t s = (cudaStream_t)stream;
-    return vec ? launch<true, true, false>(p, 1, d, s) : launch<true, false, false>(p, 1, d, s);
+    return launch<true>(p, 1, d, (cudaStream_t)stream);
 }
 
 CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch, int32_t planes,
@@ -246,7 +244,7 @@ CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch,
 static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t src_plane,
                     float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
                     int64_t plane_stride, int32_t iters, float dt, void* workspace,
-                    size_t ws_bytes, int32_t* first_bad_iter, cudaStream_t s) {
+                    int32_t* first_bad_iter, cudaStream_t s) {
     DevInfo d;
     if (int rc = device_info(&d)) return rc;
     int32_t* flag = reinterpret_cast<int32_t*>(workspace);
@@ -254,51 +252,39 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
     CF_CUDA(cudaMemsetAsync(flag, 0x7f, sizeof(int32_t), s));
 
     const std::vector<int> ks = schedule(iters);
-    const bool vec_out = pitch % 4 == 0 && (planes == 1 || plane_stride % 4 == 0) &&
-                         aligned16(out) && aligned16(ws);
-    // Ping-pong targets.  f32: src0 == out, the first launch writes ws.
-    // u8: src0 is separate; choose the first target so the last lands in out.
-    float* buf[2] = {ws, out};
-    int tgt = 0;
-    if (src_u8) tgt = (ks.size() % 2 == 1) ? 1 : 0;
-
-    const void* cur = src0;
-    bool cur_u8 = src_u8;
-    int64_t cur_pitch = src_pitch, cur_plane = src_plane;
+    // Ping-pong between the caller's buffer and the workspace, arranged so
+    // the last launch writes `out` (even launch count; iters == 1 copies).
+    float* cur = out;
+    float* nxt = ws;
+    if (src_u8) {
+        // widen u8 -> fp32 into whichever buffer makes the
+        // final launch land in `out`
+        if (ks.size() % 2 == 1) std::swap(cur, nxt);
+        dim3 grid(1184, planes);
+        u8_to_f32_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(src0), src_pitch,
+                                               src_plane, cur, pitch, plane_stride, w, h);
+        CF_CUDA(cudaGetLastError());
+    }
     int iter = 0;
     for (size_t i = 0; i < ks.size(); ++i) {
-        float* dst = buf[tgt];
         cfk::SweepParams p{};
-        p.src = cur; p.dst = dst;
-        p.src_pitch = cur_pitch; p.dst_pitch = pitch;
-        p.src_plane = cur_plane; p.dst_plane = plane_stride;
+        p.src = cur; p.dst = nxt;
+        p.src_pitch = p.dst_pitch = pitch;
+        p.src_plane = p.dst_plane = plane_stride;
         p.src_row0 = p.dst_row0 = 0;
         p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
         p.dt = dt; p.iter_base = iter; p.flag = flag;
-        int rc;
-        if (cur_u8) {
-            const bool vec = vec_out && cur_pitch % 4 == 0 && (planes == 1 || cur_plane % 4 == 0) &&
-                             ((uintptr_t)cur & 3u) == 0;
-            rc = vec ? launch<false, true, true>(p, ks[i], d, s)
-                     : launch<false, false, true>(p, ks[i], d, s);
-        } else {
-            const bool vec = vec_out && aligned16(cur);
-            rc = vec ? launch<false, true, false>(p, ks[i], d, s)
-                     : launch<false, false, false>(p, ks[i], d, s);
-        }
-        if (rc) return rc;
+        if (int rc = launch<false>(p, ks[i], d, s)) return rc;
         iter += ks[i];
-        cur = dst; cur_u8 = false; cur_pitch = pitch; cur_plane = plane_stride;
-        tgt ^= 1;
+        std::swap(cur, nxt);
     }
-    if (!src_u8 && iters == 1) {
-        // single launch wrote ws: copy U^1 back into the caller's buffer
+    if (cur != out) {
+        // iters == 1 on an in-place f32 image: the single launch wrote ws
         for (int pl = 0; pl < planes; ++pl)
-            CF_CUDA(cudaMemcpy2DAsync(out + pl * plane_stride, pitch * 4, ws + pl * plane_stride,
+            CF_CUDA(cudaMemcpy2DAsync(out + pl * plane_stride, pitch * 4, cur + pl * plane_stride,
                                       pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
     }
     if (first_bad_iter) return cf_wmc_filter_query_nonfinite(workspace, first_bad_iter, s);
-    (void)ws_bytes;
     return CF_OK;
 }
 
@@ -313,8 +299,7 @@ CF_API int cf_wmc_filter_f32(float* img, int32_t w, int32_t h, int64_t pitch, in
         workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))
         return CF_EINVAL;
     return run_flow(img, false, pitch, plane_stride, img, w, h, pitch, planes, plane_stride,
-                    iters, dt, workspace, workspace_bytes, first_bad_iter,
-                    (cudaStream_t)stream);
+                    iters, dt, workspace, first_bad_iter, (cudaStream_t)stream);
 }
 
 CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
@@ -338,7 +323,7 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
         workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))
         return CF_EINVAL;
     return run_flow(in, true, in_pitch, in_plane_stride, out, w, h, pitch, planes, plane_stride,
-                    iters, dt, workspace, workspace_bytes, first_bad_iter, s);
+                    iters, dt, workspace, first_bad_iter, s);
 }
 
 CF_API int cf_wmc_filter_query_nonfinite(const void* workspace, int32_t* first_bad_iter,
@@ -374,10 +359,7 @@ CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t sr
     p.src_row0 = src_row0; p.dst_row0 = dst_row0;
     p.w = w; p.h = h; p.y0 = y0; p.y1 = y1; p.planes = 1;
     p.dt = dt; p.iter_base = iter_base; p.flag = d_flag;
-    const bool vec = pitch % 4 == 0 && aligned16(src) && aligned16(dst);
-    cudaStream_t s = (cudaStream_t)stream;
-    return vec ? launch<false, true, false>(p, sweeps, d, s)
-               : launch<false, false, false>(p, sweeps, d, s);
+    return launch<false>(p, sweeps, d, (cudaStream_t)stream);
 }
 
 }  // extern "C"

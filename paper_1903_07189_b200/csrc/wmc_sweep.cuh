@@ -6,68 +6,68 @@
 // sweeps U <- U + dt * d_m(U) per launch, or (MAP) one evaluation of d_m.
 // Arithmetic is the canonical fp32 sequence of DESIGN.md §3 (the same
 // sequence oracle/wmc_oracle.c restates), written with explicit _rn
-// intrinsics so nvcc can neither contract nor reassociate it.
+// intrinsics / packed f32x2 PTX so nothing is contracted or reassociated.
 //
-// How: warp-streaming register blocking with packed fp32.
-//  * A warp owns column windows of 32*C columns (C adjacent columns per
-//    lane) and streams DOWN a strip of rows.  Each window overlaps its
-//    neighbours by A >= K columns per side so the K levels of the trapezoid
-//    never need another warp's data; horizontal neighbours come from warp
-//    shuffles of each produced row.
-//  * Packed fp32 across TWO column chunks: a warp owns chunk pair (2c, 2c+1);
-//    lane position j (columns xf-1 .. xf+C of each chunk) is ONE 64-bit
-//    register pair {chunk 2c value, chunk 2c+1 value}.  Every neighbour of a
-//    pixel pair is then an aligned pair, so all canonical arithmetic runs as
-//    sm_100 FFMA2/FADD2/FMUL2 (one instruction for two pixels) with no
-//    register re-layout; loads/stores are per-column 4-byte accesses that
-//    land directly in pair halves (the C accesses of a warp cover whole
-//    128-byte lines).
-//  * Level l (1..K) keeps a 3-row window of level l-1 in registers; row y of
-//    level l lives in slot y mod 3, and the step loop is unrolled by 3 so
-//    every slot index is a compile-time constant (no register moves).
-//  * Row-shared pair sums (H = l+r, T = (a+c)+(l+r)) are carried down.
-//  * Clamp-to-edge is re-applied to the CURRENT iterate at every
-//    level: rows via slot copies at rows 0 / h, columns via selects after the
-//    halo shuffle.  Only the (at most two) border warps of a row band and the
-//    prologue/epilogue steps take this checked path; interior warps run a
-//    branch-free steady state.  Level-0 rows are prefetched 3 rows ahead.
+// How:
+//  * Warp streaming.  A warp owns TWO 64-column chunks (2 adjacent columns
+//    per lane in each) and streams down a strip of rows.  Each chunk window
+//    overlaps its neighbours by A >= K columns per side, so the K levels of
+//    the trapezoid never need another warp's data.
+//  * Packed fp32 across the two chunks: column c of the warp window is ONE
+//    8-byte pair {chunk0[c], chunk1[c]}; every neighbour of a pixel pair is
+//    an aligned pair, so the whole canonical sequence runs as sm_100
+//    FFMA2/FADD2/FMUL2 (one instruction for two pixels); only the 8-way
+//    selection (FSETP+FSEL) is scalar.
+//  * Rows live in warp-private SHARED MEMORY, not registers: level 0 in a
+//    ring filled RD rows ahead by cp.async (4-byte copies land interleaved
+//    as pairs), levels 1..K-1 in 3-row rings written by the producing level.
+//    A lane reads its 4-column neighbourhood of a row with two 16-byte LDS
+//    (halo columns come from the neighbour lanes' slots -- no shuffles), so
+//    registers hold only the pixels in flight (~100 regs, high occupancy)
+//    and K can grow without register cost.
+//  * Clamp-to-edge is applied to the CURRENT iterate at every
+//    level: rows by clamping the row index of the slot read, columns by the
+//    border lanes writing the replicated value into the halo slot.
 //  * Non-finite check: one FFMA2 per pixel pair per level into
-//    a per-level accumulator; the first level whose accumulator is NaN is
-//    atomically min-ed into a device flag.  A non-finite pixel stays
-//    non-finite at every later iteration, so per-level checks
-//    of each warp's own columns name the first bad iteration exactly.
+//    a per-level accumulator (x*0 + acc is NaN iff x is not finite); the
+//    first level whose accumulator is NaN is atomically min-ed into a device
+//    flag.  A non-finite pixel stays non-finite at every later iteration
+//    (DESIGN.md §3.4), so per-level checks of each warp's own columns name
+//    the first bad iteration exactly.
 //  * MAP mode resolves opposite-sign near-ties of the selection in fp64
 //     so the map matches the fp64 SPEC evaluation to 1e-5.
 //
-// No shared memory, no block barriers: HBM traffic is one 4-byte read and one
-// 4-byte write per pixel per launch (the overlap columns hit L2).
+// HBM traffic: one 4-byte read and one 4-byte write per pixel per launch
+// (overlap columns hit L2); every other access is shared memory.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace cfk {
 
+#ifndef CF_MINB
+#define CF_MINB 4     // resident 128-thread blocks per SM the register budget targets
+#endif
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr float kC12 = 1.0f / 12.0f;  // fl(1/12)
-constexpr int C = 2;                  // columns per lane per chunk
-#ifndef CF_MINB_K2
-#define CF_MINB_K2 3
+#ifndef CF_COLS
+#define CF_COLS 2
 #endif
-#ifndef CF_PD
-#define CF_PD 3
-#endif
-#ifndef CF_CARRY
-#define CF_CARRY 0
-#endif
+constexpr int C = CF_COLS;            // columns per lane per chunk (2 or 4)
+static_assert(C == 2 || C == 4, "2 or 4 columns per lane");
+constexpr int kChunk = 32 * C;        // columns per chunk window
+constexpr int kRowBytes = 8 * (kChunk + 2);   // pairs for columns -1 .. kChunk
+constexpr int kRD = 5;                // level-0 prefetch distance (rows)
+constexpr int kRS = kRD + 3;          // level-0 ring slots (rows t-2 .. t+RD)
+static_assert((kRS & (kRS - 1)) == 0, "ring slots must be a power of two");
 
 struct SweepParams {
-    const void* src;          // global row src_row0 of plane 0 (float or uint8)
+    const float* src;         // global row src_row0 of plane 0
     float* dst;               // global row dst_row0 of plane 0
-    int64_t src_pitch;        // elements of the source type
+    int64_t src_pitch;        // elements
     int64_t dst_pitch;        // elements
-    int64_t src_plane;        // plane stride, source elements
+    int64_t src_plane;        // plane stride, elements
     int64_t dst_plane;        // plane stride, elements
     int32_t src_row0, dst_row0;
     int32_t w, h;             // global image size (clamp borders)
@@ -78,20 +78,27 @@ struct SweepParams {
     int32_t* flag;            // nullable
 };
 
-// Column geometry for K levels.
+// Column geometry for K levels: each chunk window overlaps its neighbours by
+// A = K columns per side (the trapezoid shrinks one column per level).
 template <int K>
 struct Geo {
-    static constexpr int A = ((K + C - 1) / C) * C;      // overlap per side, multiple of C
-    static constexpr int S = 32 * C - 2 * A;             // output columns per warp
-    static constexpr int LANE_LO = A / C;                // first output lane
-    static constexpr int LANE_HI = LANE_LO + S / C;      // one past last output lane
-    static_assert(A >= K && S > 0 && S % C == 0, "bad geometry");
+    static constexpr int A = K;                          // overlap per side
+    static constexpr int S = kChunk - 2 * A;             // output columns per chunk
+    static_assert(S > 0, "bad geometry");
 };
 
-// A packed pair of fp32 values held in ONE 64-bit register pair (PTX .b64),
-// operated on with sm_100 add/mul/fma.rn.f32x2 (SASS FADD2/FMUL2/FFMA2).
-// Keeping pairs as .b64 end to end avoids the per-use mov.b64 repacking that
-// float2 + __fadd2_rn produce.
+// Rings: level 0 has kRS slots (rows t-2 .. t+RD); levels 1..K-1 have 4
+// slots each (skewed pipeline).
+constexpr int kLvlSlots = 4;
+template <int K>
+__host__ __device__ constexpr int smem_bytes_per_warp() {
+    return (kRS + kLvlSlots * (K - 1)) * kRowBytes;
+}
+
+// ---------------------------------------------------------------------------
+#ifndef CF_SCALAR
+// Packed fp32 pairs in one 64-bit register pair (PTX .b64) and sm_100
+// add/mul/fma.rn.f32x2 (SASS FADD2/FMUL2/FFMA2).
 using f2 = unsigned long long;
 __device__ __forceinline__ f2 add2(f2 a, f2 b) {
     f2 d;
@@ -123,46 +130,70 @@ __device__ __forceinline__ float hi(f2 v) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
     return b;
 }
-__device__ __forceinline__ constexpr f2 splat_bits(uint32_t b) { return ((f2)b << 32) | b; }
+#define CF_PAIR_CONST(lo32) (((unsigned long long)(lo32) << 32) | (unsigned long long)(lo32))
+#else
+// Scalar build of the same sequence (two independent fp32 lanes).
+struct f2 {
+    float x, y;
+};
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { return {__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)}; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return {__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)}; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    return {__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y)};
+}
+__device__ __forceinline__ f2 pk(float lo, float hi) { return {lo, hi}; }
+__device__ __forceinline__ float lo(f2 v) { return v.x; }
+__device__ __forceinline__ float hi(f2 v) { return v.y; }
+#endif
 __device__ __forceinline__ f2 splat(float v) { return pk(v, v); }
+#ifndef CF_SCALAR
 constexpr f2 kTwo2 = 0x4000000040000000ull;    // {2, 2}
 constexpr f2 kFour2 = 0x4080000040800000ull;   // {4, 4}
 constexpr f2 kM12x2 = 0xC1400000C1400000ull;   // {-12, -12}
 constexpr f2 kC12x2 = 0x3DAAAAAB3DAAAAABull;   // {fl(1/12), fl(1/12)}
 constexpr f2 kZero2 = 0ull;
+#else
+constexpr f2 kTwo2 = {2.0f, 2.0f};
+constexpr f2 kFour2 = {4.0f, 4.0f};
+constexpr f2 kM12x2 = {-12.0f, -12.0f};
+constexpr f2 kC12x2 = {1.0f / 12.0f, 1.0f / 12.0f};
+constexpr f2 kZero2 = {0.0f, 0.0f};
+#endif
 
-// Level-0 prefetch ring (f32 inputs): each lane cp.async-copies its 2*C
-// input values of row t+RD into shared memory, interleaved as
-// {chunk0 col j, chunk1 col j} so that one 16-byte LDS returns the pairs
-// ready for FFMA2.  No registers are held for in-flight rows.
-constexpr int kRingRows = 8;
-constexpr int kRingBytesPerWarp = kRingRows * 32 * 16;
-
+// ---- shared memory / async copy helpers ----------------------------------
 __device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void cp_async_wait_rd() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kRD - 1) : "memory");
 }
-
-// One window row: positions p0..p5 (columns xf-1 .. xf+4), each a pair
-// {chunk 2c, chunk 2c+1}.
-struct Row {
-    f2 q[C + 2];
-};
-
-// A prefetched level-0 row, kept as 32-bit scalars (chunk 0 in a, chunk 1
-// in b) so the loads land in their own registers; they are packed into
-// pairs only when consumed PD steps later.
-struct Staged {
-    float a[C], b[C];
-};
-
-struct Carry {
-    f2 hc[C], tm[C];  // H(y) = l+r and T(y-1) = (a+c)+(l+r) of pixels p1..pC
-};
+// The C+2 pairs (columns C*i-1 .. C*i+C) a lane needs from one row, read
+// with 16-byte LDS from byte a = row + 8*C*i (16-aligned).
+__device__ __forceinline__ void lds_nb(uint32_t a, f2 (&q)[C + 2]) {
+#pragma unroll
+    for (int k = 0; k < (C + 2) / 2; ++k) {
+#ifndef CF_SCALAR
+        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                     : "=l"(q[2 * k]), "=l"(q[2 * k + 1]) : "r"(a + 16 * k));
+#else
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(q[2 * k].x), "=f"(q[2 * k].y), "=f"(q[2 * k + 1].x),
+                       "=f"(q[2 * k + 1].y) : "r"(a + 16 * k));
+#endif
+    }
+}
+// Store one pair at byte a (8-aligned).
+__device__ __forceinline__ void sts_pair(uint32_t a, f2 v) {
+#ifndef CF_SCALAR
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+#else
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+#endif
+}
+__device__ __forceinline__ void sts1(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
 
 // first-minimum of |.|: a tournament with the left operand
 // winning ties; for finite inputs identical to the strict-< scan 1..8.
@@ -178,24 +209,23 @@ struct PairD {
     f2 n12u;
 };
 
+// Row-shared sums are carried down a level: Hc = l+r and Tm = (a+c)+(l+r) of
+// this row come from the row above (Hb, T0 there); Hb, T0 are returned.
 __device__ __forceinline__ void pair_d(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f, f2 g,
-                                       f2 Wm, f2 W0, f2 Hc, f2 Tm, f2& Hb_out, f2& T0_out,
-                                       PairD& P) {
+                                       f2 Wm, f2 W0, f2 Hc, f2 Tm, f2& Hb, f2& T0, PairD& P) {
     const f2 two = kTwo2, four = kFour2;
     P.n12u = mul2(u, kM12x2);
-    const f2 Hb = add2(e, g);
-    const f2 T0 = add2(Hc, Hb);
+    Hb = add2(e, g);                          // e+g
+    T0 = add2(Hc, Hb);                        // (l+r)+(e+g)
     P.d[0] = fma2(two, fma2(two, l, Wm), P.n12u);
     P.d[1] = fma2(two, fma2(two, b, Tm), P.n12u);
     P.d[2] = fma2(two, fma2(two, r, W0), P.n12u);
     P.d[3] = fma2(two, fma2(two, f, T0), P.n12u);
-    const f2 K5 = add2(c, e), K6 = add2(a, g);
-    P.d[4] = add2(fma2(four, add2(b, l), fma2(two, a, K5)), P.n12u);
-    P.d[5] = add2(fma2(four, add2(b, r), fma2(two, c, K6)), P.n12u);
-    P.d[6] = add2(fma2(four, add2(r, f), fma2(two, g, K5)), P.n12u);
-    P.d[7] = add2(fma2(four, add2(l, f), fma2(two, e, K6)), P.n12u);
-    Hb_out = Hb;
-    T0_out = T0;
+    const f2 K5 = add2(add2(c, e), P.n12u), K6 = add2(add2(a, g), P.n12u);
+    P.d[4] = fma2(four, add2(b, l), fma2(two, a, K5));
+    P.d[5] = fma2(four, add2(b, r), fma2(two, c, K6));
+    P.d[6] = fma2(four, add2(r, f), fma2(two, g, K5));
+    P.d[7] = fma2(four, add2(l, f), fma2(two, e, K6));
 }
 
 __device__ __forceinline__ f2 select_pair(const PairD& P) {
@@ -245,325 +275,298 @@ __device__ __noinline__ float wmc_px_f64(float a, float b, float c, float l, flo
     return __double2float_rn(best);
 }
 
-template <int K, bool MAP, bool VEC, bool U8>
+// ---------------------------------------------------------------------------
+template <int K, bool MAP>
 struct SweepWarp {
     using G = Geo<K>;
-    static constexpr int NL = K;  // windows for levels 0..K-1
-    static constexpr int PD = CF_PD;  // level-0 prefetch distance (rows): 1 or 3
 
     const SweepParams& P;
     int lane;
     int xf[2];                    // first column of this lane in each chunk
-    bool out_lane;                // lane holds output columns
-    bool out_h[2];                // chunk h exists (second chunk may be past w)
+    bool outc[C];                 // column j of this lane is an output column
+    bool out_h[2];                // chunk h exists (a missing chunk is never stored)
     bool border;                  // some window touches column 0 or w-1 (uniform)
-    bool clampL[2];               // this lane holds column 0 (per chunk)
-    int clampR[2];                // position (1..4) holding column w-1, else 0
     int ys, ye;                   // output strip rows
-    int rlo[K + 1], rhi[K + 1];   // rows computed per level
-    const unsigned char* srcp;    // plane base (bytes)
+    // rows computed per level L: [rlo(L), rhi(L)) (recomputed, not stored)
+    __device__ __forceinline__ int rlo(int L) const { return max(ys - (K - L), 0); }
+    __device__ __forceinline__ int rhi(int L) const { return min(ye + (K - L), P.h); }
+    const float* srcp;            // plane base
     float* dstp;                  // plane base
-
-    Row win[NL][3];
-    Carry cr[K + 1];
-    Staged stage[U8 ? PD : 1];     // u8 inputs: register prefetch
-    uint32_t ring;                 // f32 inputs: shared address of this lane's ring row 0
-    int rslot;                     // ring slot of the row consumed at the current step
+    uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     f2 acc[K + 1];
+    f2 hc[K + 1][C], tm[K + 1][C];  // carried row sums per level and pixel pair
+    f2 onv[K + 1][C];               // results of the current step, per level
 
     __device__ __forceinline__ SweepWarp(const SweepParams& p) : P(p) {}
 
-    static __device__ __forceinline__ constexpr int md3(int r) { return ((r % 3) + 3) % 3; }
+    // Skewed pipeline: level L at step t computes row t - (2L - 1), reading
+    // only rows its predecessor produced at earlier steps, so the K level
+    // computations of one step are independent (K-way ILP, one __syncwarp
+    // per step).
+    static __device__ __forceinline__ constexpr int lag(int L) { return 2 * L - 1; }
 
-    // ---- level-0 loads (raw; widening handled at consume time) ----------
-    __device__ __forceinline__ const unsigned char* src_row(int y) const {
-        return srcp + (int64_t)(y - P.src_row0) * P.src_pitch * (U8 ? 1 : 4);
-    }
-    __device__ __forceinline__ float* dst_row(int y) const {
-        return dstp + (int64_t)(y - P.dst_row0) * P.dst_pitch;
+    // shared address of row y of level L (row index clamped to [0, h):
+    // clamp-to-edge on the current iterate).
+    template <int L>
+    __device__ __forceinline__ uint32_t row_addr(int y) const {
+        y = min(max(y, 0), P.h - 1);
+        if constexpr (L == 0) {
+            return sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes;
+        } else {
+            return sbase + (uint32_t)(kRS + kLvlSlots * (L - 1) + (y & (kLvlSlots - 1))) *
+                               kRowBytes;
+        }
     }
 
-    // CHECKED: rowp is the row start, columns clamped to [0, w).
-    // fast:    rowp already points at column xf[0]; chunk 1 is G::S columns on.
-    template <bool CHECKED>
-    __device__ __forceinline__ Staged load_row(const unsigned char* rowp) const {
-        Staged st;
+    // cp.async this lane's 4 input values of row y into ring slot y % kRS:
+    // column c of chunk h lands at byte 8*(c+1) + 4*h of the row.
+    __device__ __forceinline__ void prefetch(int y) const {
+        const float* row = srcp + (int64_t)(y - P.src_row0) * P.src_pitch;
+        const uint32_t s = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
 #pragma unroll
         for (int j = 0; j < C; ++j) {
-            int x0 = j, x1 = G::S + j;  // fast: rowp points at column xf[0]
-            if (CHECKED) {
-                x0 = min(max(xf[0] + j, 0), P.w - 1);
-                x1 = min(max(xf[1] + j, 0), P.w - 1);
+            int x0 = xf[0] + j, x1 = xf[1] + j;
+            if (border) {
+                x0 = min(max(x0, 0), P.w - 1);
+                x1 = min(max(x1, 0), P.w - 1);
             }
-            if constexpr (U8) {
-                st.a[j] = __uint_as_float((uint32_t)__ldg(rowp + x0));
-                st.b[j] = __uint_as_float((uint32_t)__ldg(rowp + x1));
-            } else {
-                const float* row = reinterpret_cast<const float*>(rowp);
-                st.a[j] = __ldg(row + x0);
-                st.b[j] = __ldg(row + x1);
-            }
-        }
-        return st;
-    }
-
-    // f32 prefetch: copy this lane's values of one row into ring slot `slot`.
-    template <bool CHECKED>
-    __device__ __forceinline__ void ring_issue(const unsigned char* rowp, int slot) const {
-        const float* row = reinterpret_cast<const float*>(rowp);
-        const uint32_t sa = ring + (uint32_t)slot * (32 * 16);
-#pragma unroll
-        for (int j = 0; j < C; ++j) {
-            int x0 = j, x1 = G::S + j;  // fast: rowp points at column xf[0]
-            if (CHECKED) {
-                x0 = min(max(xf[0] + j, 0), P.w - 1);
-                x1 = min(max(xf[1] + j, 0), P.w - 1);
-            }
-            cp_async4(sa + 8 * j, row + x0);
-            cp_async4(sa + 8 * j + 4, row + x1);
-        }
-        cp_async_commit();
-    }
-    __device__ __forceinline__ void ring_consume(int slot, f2 (&v)[C]) const {
-        static_assert(C == 2, "ring rows hold 2 pairs per lane");
-        const uint32_t sa = ring + (uint32_t)slot * (32 * 16);
-        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "r"(sa));
-    }
-
-    __device__ __forceinline__ f2 widen(float a, float b) const {
-        if constexpr (U8) {  // (float)q / 255 in IEEE fp32
-            return pk(__fdiv_rn((float)__float_as_uint(a), 255.0f),
-                      __fdiv_rn((float)__float_as_uint(b), 255.0f));
-        } else {
-            return pk(a, b);
+            cp_async4(s + 8 * j, row + x0);
+            cp_async4(s + 8 * j + 4, row + x1);
         }
     }
 
-    // Build a window row from the lane's positions p1..p4: halo shuffles,
-    // then (CLAMP) clamp-to-edge at the image's first/last column.
-    template <bool CLAMP>
-    __device__ __forceinline__ void make_row(Row& R, const f2 (&v)[C]) const {
+    // Border lanes replicate column 0 into column -1 and column w-1 into
+    // column w of a freshly written row (per chunk half).
+    __device__ __forceinline__ void clamp_row(uint32_t rowbase) const {
 #pragma unroll
-        for (int j = 0; j < C; ++j) R.q[j + 1] = v[j];
-        const float l0 = __shfl_up_sync(kFull, lo(v[C - 1]), 1);  // left lane's pC
-        const float l1 = __shfl_up_sync(kFull, hi(v[C - 1]), 1);
-        const float r0 = __shfl_down_sync(kFull, lo(v[0]), 1);  // right lane's p1
-        const float r1 = __shfl_down_sync(kFull, hi(v[0]), 1);
-        R.q[0] = pk(l0, l1);
-        R.q[C + 1] = pk(r0, r1);
-        if constexpr (CLAMP) {
-            float a[C + 2], b[C + 2];
+        for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int i = 0; i < C + 2; ++i) { a[i] = lo(R.q[i]); b[i] = hi(R.q[i]); }
-            if (clampL[0]) a[0] = a[1];
-            if (clampL[1]) b[0] = b[1];
-#pragma unroll
-            for (int i = 1; i <= C; ++i) {
-                if (clampR[0] == i) a[i + 1] = a[i];
-                if (clampR[1] == i) b[i + 1] = b[i];
-            }
-            // columns >= w hold pitch padding or clamped loads: keep finite
-#pragma unroll
-            for (int i = 1; i <= C; ++i) {
-                if (xf[0] + i - 1 > P.w) a[i] = 0.0f;
-                if (xf[1] + i - 1 > P.w) b[i] = 0.0f;
-            }
-#pragma unroll
-            for (int i = 0; i < C + 2; ++i) R.q[i] = pk(a[i], b[i]);
-        }
-    }
-
-    // ---- level 0 of one step: consume the prefetched row, prefetch ahead --
-    template <int PH, bool CHECKED>
-    __device__ __forceinline__ void level0(int t, const unsigned char*& lptr) {
-        constexpr int s_y = md3(PH), s_ym = md3(PH - 1);
-        f2 v[C];
-        if constexpr (!U8) {
-            cp_async_wait<kRingRows - 1>();        // row t has landed
-            ring_consume(rslot, v);
-        }
-        if (!CHECKED || (t >= rlo[0] && t < rhi[0])) {
-            if constexpr (U8) {
-#pragma unroll
-                for (int j = 0; j < C; ++j)
-                    v[j] = widen(stage[PH % PD].a[j], stage[PH % PD].b[j]);
-            }
-            make_row<CHECKED>(win[0][s_y], v);
-            if (CHECKED && t == 0) win[0][s_ym] = win[0][s_y];  // row -1 := row 0
-        } else if (CHECKED && t == P.h && rhi[0] == P.h) {
-            win[0][s_y] = win[0][s_ym];                          // row h := row h-1
-        }
-        constexpr int AHEAD = U8 ? PD : kRingRows;
-        if constexpr (U8) {
-            if (CHECKED) {
-                stage[PH % PD] = load_row<true>(src_row(min(max(t + PD, rlo[0]), rhi[0] - 1)));
-            } else {
-                stage[PH % PD] = load_row<false>(lptr);  // row t + PD
-                lptr += P.src_pitch;
-            }
-        } else {
-            if (CHECKED) {
-                ring_issue<true>(src_row(min(max(t + AHEAD, rlo[0]), rhi[0] - 1)), rslot);
-            } else {
-                ring_issue<false>(lptr, rslot);          // row t + kRingRows
-                lptr += P.src_pitch * 4;
-            }
-            rslot = rslot + 1 == kRingRows ? 0 : rslot + 1;
-        }
-    }
-
-    // ---- level L >= 1 of one step ---------------------------------------
-    template <int PH, int L, bool CHECKED>
-    __device__ __forceinline__ void level(int t, float*& sptr) {
-        const int y = t - L;
-        constexpr int s_y = md3(PH - L);        // slot of row y
-        constexpr int s_ym = md3(PH - L - 1);   // slot of row y-1
-        constexpr int s_yp = md3(PH - L + 1);   // slot of row y+1
-        if (!CHECKED || (y >= rlo[L] && y < rhi[L])) {
-            const f2 (&m)[C + 2] = win[L - 1][s_ym].q;
-            const f2 (&o)[C + 2] = win[L - 1][s_y].q;
-            const f2 (&p)[C + 2] = win[L - 1][s_yp].q;
-            Carry& cc = cr[L];
-            if ((CHECKED && y == rlo[L]) || !CF_CARRY) {
-#pragma unroll
-                for (int j = 1; j <= C; ++j) {
-                    cc.hc[j - 1] = add2(o[j - 1], o[j + 1]);                       // l + r
-                    cc.tm[j - 1] = add2(add2(m[j - 1], m[j + 1]), cc.hc[j - 1]);  // (a+c)+(l+r)
+            for (int j = 0; j < C; ++j) {
+                const int x = xf[h] + j;
+                const int c = lane * C + j;  // window column
+                const uint32_t a = rowbase + 8 * (c + 1) + 4 * h;
+                float v;
+                if (x == 0) {
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+                    sts1(a - 8, v);
+                }
+                if (x == P.w - 1) {
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+                    sts1(a + 8, v);
                 }
             }
-            f2 V[C + 2];
-#pragma unroll
-            for (int i = 0; i < C + 2; ++i) V[i] = add2(m[i], p[i]);              // a+e / b+f / c+g
-            f2 W[C + 1];
-#pragma unroll
-            for (int i = 0; i < C + 1; ++i) W[i] = add2(V[i], V[i + 1]);          // (a+e)+(b+f)
-            f2 nv[C];
+        }
+    }
+
+    // Compute level L's row for step t.  CHECKED: range check, clamped row
+    // indices, predicated stores.  Fast: steady state, rows via R4[] (slot
+    // offsets of rows t+c, c = 0..3, in the 4-slot rings) and r0[] (level-0
+    // ring rows t-2, t-1, t).  Results are stored (STS / STG) but not yet
+    // visible to other lanes: the caller syncs once per step.
+    template <int L, bool CHECKED>
+    __device__ __forceinline__ void level(int t, const uint32_t (&R4)[4], const uint32_t (&r0)[3],
+                                          float* sptr) {
+        const int y = t - lag(L);
+        if (CHECKED && (y < rlo(L) || y >= rhi(L))) return;  // warp-uniform
+        uint32_t am, ao, ap;
+        if constexpr (CHECKED) {
+            am = row_addr<L - 1>(y - 1);
+            ao = row_addr<L - 1>(y);
+            ap = row_addr<L - 1>(y + 1);
+        } else if constexpr (L == 1) {
+            am = r0[0]; ao = r0[1]; ap = r0[2];
+        } else {
+            // level L-1 row r in slot r & 3; rows y-1, y, y+1 = t - 2L + k
+            const uint32_t rb = sbase + (uint32_t)(kRS + kLvlSlots * (L - 2)) * kRowBytes;
+            am = rb + R4[(-2 * L + 0 + 64) & 3];
+            ao = rb + R4[(-2 * L + 1 + 64) & 3];
+            ap = rb + R4[(-2 * L + 2 + 64) & 3];
+        }
+        f2 m[C + 2], o[C + 2], p[C + 2];
+        lds_nb(am + 8 * C * lane, m);
+        lds_nb(ao + 8 * C * lane, o);
+        lds_nb(ap + 8 * C * lane, p);
+        if (CHECKED && y == rlo(L)) {  // first row of this level: no carries yet
 #pragma unroll
             for (int j = 1; j <= C; ++j) {
-                PairD D;
-                f2 hb, t0;
-                pair_d(m[j - 1], m[j], m[j + 1], o[j - 1], o[j], o[j + 1], p[j - 1], p[j],
-                       p[j + 1], W[j - 1], W[j], cc.hc[j - 1], cc.tm[j - 1], hb, t0, D);
-                cc.hc[j - 1] = hb;
-                cc.tm[j - 1] = t0;
-                const f2 b = select_pair(D);
-                f2 hw = mul2(b, kC12x2);
-                if constexpr (MAP) {
-                    const bool t0_ = near_tie(D, 0, lo(b)), t1_ = near_tie(D, 1, hi(b));
-                    if (__any_sync(kFull, t0_ | t1_)) {
-                        float h0 = lo(hw), h1 = hi(hw);
-                        if (t0_) h0 = wmc_px_f64(lo(m[j - 1]), lo(m[j]), lo(m[j + 1]),
-                                                 lo(o[j - 1]), lo(o[j]), lo(o[j + 1]),
-                                                 lo(p[j - 1]), lo(p[j]), lo(p[j + 1]));
-                        if (t1_) h1 = wmc_px_f64(hi(m[j - 1]), hi(m[j]), hi(m[j + 1]),
-                                                 hi(o[j - 1]), hi(o[j]), hi(o[j + 1]),
-                                                 hi(p[j - 1]), hi(p[j]), hi(p[j + 1]));
-                        hw = pk(h0, h1);
-                    }
-                    nv[j - 1] = hw;
-                } else {
-                    nv[j - 1] = fma2(splat(P.dt), hw, o[j]);   // u + dt * H^w
-                    acc[L] = fma2(nv[j - 1], kZero2, acc[L]);
-                }
+                hc[L][j - 1] = add2(o[j - 1], o[j + 1]);                        // l+r
+                tm[L][j - 1] = add2(add2(m[j - 1], m[j + 1]), hc[L][j - 1]);   // (a+c)+(l+r)
             }
-            if constexpr (L == K) {
-                if (CHECKED) {
-                    store_row<true>(dst_row(y), nv);
-                } else {
-                    store_row<false>(sptr, nv);  // row t - K
-                    sptr += P.dst_pitch;
-                }
-            } else {
-                make_row<CHECKED>(win[L][s_y], nv);
-                if (CHECKED && y == 0) win[L][s_ym] = win[L][s_y];
-            }
-        } else if constexpr (L < K) {
-            if (y == P.h && rhi[L] == P.h) win[L][s_y] = win[L][s_ym];
         }
-    }
-
-    // CHECKED: row is the row start; fast: row points at column xf[0].
-    template <bool CHECKED>
-    __device__ __forceinline__ void store_row(float* row, const f2 (&nv)[C]) const {
-        if (!out_lane) return;
+        f2 V[C + 2], W[C + 1];
 #pragma unroll
-        for (int j = 0; j < C; ++j) {
-            if (CHECKED) {
-                if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = lo(nv[j]);
-                if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = hi(nv[j]);
+        for (int i = 0; i < C + 2; ++i) V[i] = add2(m[i], p[i]);  // a+e / b+f / c+g
+#pragma unroll
+        for (int i = 0; i < C + 1; ++i) W[i] = add2(V[i], V[i + 1]);  // (a+e)+(b+f)
+        f2 nv[C];
+#pragma unroll
+        for (int j = 1; j <= C; ++j) {
+            PairD D;
+            f2 hb, t0;
+            pair_d(m[j - 1], m[j], m[j + 1], o[j - 1], o[j], o[j + 1], p[j - 1], p[j], p[j + 1],
+                   W[j - 1], W[j],
+                   hc[L][j - 1], tm[L][j - 1], hb, t0, D);
+            hc[L][j - 1] = hb;
+            tm[L][j - 1] = t0;
+            const f2 b = select_pair(D);
+            f2 hw = mul2(b, kC12x2);
+            if constexpr (MAP) {
+                const bool t0 = near_tie(D, 0, lo(b)), t1 = near_tie(D, 1, hi(b));
+                if (__any_sync(kFull, t0 | t1)) {
+                    float h0 = lo(hw), h1 = hi(hw);
+                    if (t0) h0 = wmc_px_f64(lo(m[j - 1]), lo(m[j]), lo(m[j + 1]), lo(o[j - 1]),
+                                            lo(o[j]), lo(o[j + 1]), lo(p[j - 1]), lo(p[j]),
+                                            lo(p[j + 1]));
+                    if (t1) h1 = wmc_px_f64(hi(m[j - 1]), hi(m[j]), hi(m[j + 1]), hi(o[j - 1]),
+                                            hi(o[j]), hi(o[j + 1]), hi(p[j - 1]), hi(p[j]),
+                                            hi(p[j + 1]));
+                    hw = pk(h0, h1);
+                }
+                nv[j - 1] = hw;
             } else {
-                row[j] = lo(nv[j]);
-                row[G::S + j] = hi(nv[j]);
+                nv[j - 1] = fma2(splat(P.dt), hw, o[j]);   // u + dt * H^w
+                if (outc[j - 1]) acc[L] = fma2(nv[j - 1], kZero2, acc[L]);
             }
+        }
+#pragma unroll
+        for (int j = 0; j < C; ++j) onv[L][j] = nv[j];
+    }
+
+    // Store phase of a step (after every level computed, so no shared-memory
+    // store precedes a later level's loads: the compiler is free to overlap
+    // the K independent level computations).
+    template <int L, bool CHECKED>
+    __device__ __forceinline__ void store(int t, const uint32_t (&R4)[4], float* sptr) {
+        store_one<L, CHECKED>(t, R4, sptr);
+        if constexpr (L < K) store<L + 1, CHECKED>(t, R4, sptr);
+    }
+
+    template <int L, bool CHECKED>
+    __device__ __forceinline__ void store_one(int t, const uint32_t (&R4)[4], float* sptr) {
+        const int y = t - lag(L);
+        if (CHECKED && (y < rlo(L) || y >= rhi(L))) return;  // warp-uniform
+        const f2 (&nv)[C] = onv[L];
+        if constexpr (L == K) {
+            if (CHECKED) {
+                float* row = dstp + (int64_t)(y - P.dst_row0) * P.dst_pitch;
+#pragma unroll
+                for (int j = 0; j < C; ++j) {
+                    if (!outc[j]) continue;
+                    if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = lo(nv[j]);
+                    if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = hi(nv[j]);
+                }
+            } else {  // sptr: row y at column xf[0]; chunk 1 is G::S columns on
+#pragma unroll
+                for (int j = 0; j < C; ++j) {
+                    if (!outc[j]) continue;
+                    sptr[j] = lo(nv[j]);
+                    sptr[G::S + j] = hi(nv[j]);
+                }
+            }
+        } else {
+            uint32_t rb;
+            if constexpr (CHECKED) {
+                rb = row_addr<L>(y);
+            } else {  // row y = t - 2L + 1 in slot y & 3
+                rb = sbase + (uint32_t)(kRS + kLvlSlots * (L - 1)) * kRowBytes +
+                     R4[(-2 * L + 1 + 64) & 3];
+            }
+#pragma unroll
+            for (int j = 0; j < C; ++j) sts_pair(rb + 8 * C * lane + 8 + 8 * j, nv[j]);
         }
     }
 
-    template <int PH, int L, bool CHECKED>
-    __device__ __forceinline__ void levels(int t, float*& sptr) {
-        level<PH, L, CHECKED>(t, sptr);
-        if constexpr (L < K) levels<PH, L + 1, CHECKED>(t, sptr);
+    template <int L, bool CHECKED>
+    __device__ __forceinline__ void levels(int t, const uint32_t (&R4)[4],
+                                           const uint32_t (&r0)[3], float* sptr) {
+        level<L, CHECKED>(t, R4, r0, sptr);
+        if constexpr (L < K) levels<L + 1, CHECKED>(t, R4, r0, sptr);
     }
 
-    template <int PH, bool CHECKED>
-    __device__ __forceinline__ void step(int t, int t_begin, int t_end,
-                                         const unsigned char*& lptr, float*& sptr) {
-        level0<PH, CHECKED>(t, lptr);  // prefetch keeps running even for skipped steps
-        if (CHECKED && (t < t_begin || t > t_end)) return;
-        levels<PH, 1, CHECKED>(t, sptr);
+    // Border warps: replicate the edge columns of every row written this step.
+    template <int L>
+    __device__ __forceinline__ void clamp_levels(int t) {
+        const int y = t - lag(L);
+        if (y >= rlo(L) && y < rhi(L)) clamp_row(row_addr<L>(y));
+        if constexpr (L + 1 < K) clamp_levels<L + 1>(t);
     }
 
     __device__ __forceinline__ void run() {
-        const int t_begin = rlo[0];
-        const int t_end = ye - 1 + K;
-        // steady steps: every level past its first row, no clamp copies,
-        // prefetch in range, no clamp columns
-        const int t_s = border ? 0x7fffffff : ys + K + 1;
-        constexpr int AHEAD = U8 ? PD : kRingRows;
-        const int t_e = min(ye + K, P.h) - 1 - AHEAD;
+        const int t_begin = rlo(0);
+        const int t_end = ye - 1 + lag(K);
+        // steady steps: every level in range with unclamped neighbour rows,
+        // interior warp
+        int t_s = border ? 0x7fffffff : 0, t_e = rhi(0) - 1;
+#pragma unroll
+        for (int L = 1; L <= K; ++L) {
+            t_s = max(t_s, max(rlo(L) + 1, 1) + lag(L));    // y-1 >= 0, y > rlo (carries)
+            t_e = min(t_e, min(rhi(L) - 1, P.h - 2) + lag(L));  // y+1 <= h-1, y < rhi
+        }
 #pragma unroll
         for (int L = 0; L <= K; ++L) acc[L] = kZero2;
-        const int tb0 = t_begin - t_begin % 3;
+        // prologue: rows t_begin .. t_begin+RD-1 (one commit group per row)
 #pragma unroll
-        for (int i = 0; i < AHEAD; ++i) {
-            const unsigned char* rp = src_row(min(max(tb0 + i, rlo[0]), rhi[0] - 1));
-            if constexpr (U8) stage[i] = load_row<true>(rp);
-            else              ring_issue<true>(rp, i);
+        for (int i = 0; i < kRD; ++i) {
+            const int y = t_begin + i;
+            if (y < rhi(0)) prefetch(y);
+            cp_async_commit();
         }
-        rslot = 0;
-        const unsigned char* lptr = nullptr;
-        float* sptr = nullptr;
-        bool fast_prev = false;
-        for (int tb = tb0; tb <= t_end; tb += 3) {
-            if (tb >= t_s && tb + 2 <= t_e) {
-                if (!fast_prev) {  // (re)seed the running row pointers (at column xf[0])
-                    lptr = src_row(tb + AHEAD) + (int64_t)xf[0] * (U8 ? 1 : 4);
-                    sptr = dst_row(tb - K) + xf[0];
-                    fast_prev = true;
-                }
-                step<0, false>(tb, t_begin, t_end, lptr, sptr);
-                step<1, false>(tb + 1, t_begin, t_end, lptr, sptr);
-                step<2, false>(tb + 2, t_begin, t_end, lptr, sptr);
-            } else {
-                fast_prev = false;
-                step<0, true>(tb, t_begin, t_end, lptr, sptr);
-                step<1, true>(tb + 1, t_begin, t_end, lptr, sptr);
-                step<2, true>(tb + 2, t_begin, t_end, lptr, sptr);
+        // running pointers: prefetch source (row t+RD, column xf[0]) and the
+        // level-K store row (t - lag(K), column xf[0])
+        const float* lptr = srcp + (int64_t)(t_begin + kRD - P.src_row0) * P.src_pitch + xf[0];
+        float* sptr = dstp + (int64_t)(t_begin - lag(K) - P.dst_row0) * P.dst_pitch + xf[0];
+        for (int t = t_begin; t <= t_end; ++t) {
+            cp_async_wait_rd();       // this lane's copies of row t landed
+            if (border) {
+                __syncwarp();
+                if (t < rhi(0)) clamp_row(row_addr<0>(t));
             }
+            __syncwarp();             // rows of step t-1 and row t visible to all lanes
+            if (t + kRD < rhi(0)) {
+                if (!border) {
+                    const uint32_t sa =
+                        sbase + (uint32_t)((t + kRD) & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
+#pragma unroll
+                    for (int j = 0; j < C; ++j) {
+                        cp_async4(sa + 8 * j, lptr + j);
+                        cp_async4(sa + 8 * j + 4, lptr + G::S + j);
+                    }
+                } else {
+                    prefetch(t + kRD);
+                }
+            }
+            lptr += P.src_pitch;
+            cp_async_commit();
+            const uint32_t R4[4] = {(uint32_t)(t & 3) * kRowBytes,
+                                    (uint32_t)((t + 1) & 3) * kRowBytes,
+                                    (uint32_t)((t + 2) & 3) * kRowBytes,
+                                    (uint32_t)((t + 3) & 3) * kRowBytes};
+            if (t >= t_s && t <= t_e) {
+                const uint32_t r0[3] = {sbase + (uint32_t)((t - 2) & (kRS - 1)) * kRowBytes,
+                                        sbase + (uint32_t)((t - 1) & (kRS - 1)) * kRowBytes,
+                                        sbase + (uint32_t)(t & (kRS - 1)) * kRowBytes};
+                levels<1, false>(t, R4, r0, sptr);
+                store<1, false>(t, R4, sptr);
+            } else {
+                const uint32_t r0[3] = {0, 0, 0};
+                levels<1, true>(t, R4, r0, sptr);
+                store<1, true>(t, R4, sptr);
+                if constexpr (K > 1) {
+                    if (border) {
+                        __syncwarp();
+                        clamp_levels<1>(t);
+                    }
+                }
+            }
+            sptr += P.dst_pitch;
         }
     }
 };
 
-// Resident blocks per SM the register allocation is held to (occupancy vs
-// spills; measured): 16 warps/SM for K <= 2, 12 for K = 3.
-template <int K>
-struct MinBlocks {
-    static constexpr int value = K <= 2 ? CF_MINB_K2 : (K == 3 ? 3 : 2);
-};
-
-template <int K, bool MAP, bool VEC, bool U8>
-__global__ void __launch_bounds__(kThreads, MinBlocks<K>::value)
-    wmc_sweeps_kernel(const SweepParams p) {
+template <int K, bool MAP>
+__global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const SweepParams p) {
     using G = Geo<K>;
+    extern __shared__ __align__(16) unsigned char smem[];
     const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     const int n_pairs = (p.n_chunks + 1) / 2;
     const int total = n_pairs * p.n_strips * p.planes;
@@ -573,9 +576,13 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<K>::value)
     const int strip = rest % p.n_strips;
     const int plane = rest / p.n_strips;
 
-    SweepWarp<K, MAP, VEC, U8> sw(p);
+    SweepWarp<K, MAP> sw(p);
     sw.lane = threadIdx.x & 31;
-    sw.out_lane = sw.lane >= G::LANE_LO && sw.lane < G::LANE_HI;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+        const int c = sw.lane * C + j;  // window column
+        sw.outc[j] = c >= G::A && c < G::A + G::S;
+    }
     sw.border = false;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -584,26 +591,15 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<K>::value)
         sw.out_h[h] = chunk < p.n_chunks;
         // a missing second chunk mirrors the first (finite data, never stored)
         sw.xf[h] = (sw.out_h[h] ? xs : xs - G::S) + sw.lane * C;
-        sw.border |= xs < 0 || xs + 32 * C > p.w || !sw.out_h[h];
-        sw.clampL[h] = sw.xf[h] == 0;
-        sw.clampR[h] = (p.w - 1 >= sw.xf[h] && p.w - 1 < sw.xf[h] + C) ? p.w - sw.xf[h] : 0;
+        sw.border |= xs < 0 || xs + kChunk > p.w || !sw.out_h[h];
     }
     sw.ys = p.y0 + strip * p.strip_rows;
     sw.ye = min(sw.ys + p.strip_rows, p.y1);
     if (sw.ys >= sw.ye) return;
-#pragma unroll
-    for (int L = 0; L <= K; ++L) {
-        sw.rlo[L] = max(sw.ys - (K - L), 0);
-        sw.rhi[L] = min(sw.ye + (K - L), p.h);
-    }
-    const int esz = U8 ? 1 : 4;
-    sw.srcp = reinterpret_cast<const unsigned char*>(p.src) + (int64_t)plane * p.src_plane * esz;
-    if constexpr (!U8) {
-        extern __shared__ __align__(16) unsigned char smem_ring[];
-        sw.ring = (uint32_t)__cvta_generic_to_shared(smem_ring) +
-                  (uint32_t)(threadIdx.x >> 5) * kRingBytesPerWarp + (uint32_t)sw.lane * 16;
-    }
+    sw.srcp = p.src + (int64_t)plane * p.src_plane;
     sw.dstp = p.dst + (int64_t)plane * p.dst_plane;
+    sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
+               (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K>();
 
     sw.run();
 
@@ -613,7 +609,8 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<K>::value)
 #pragma unroll
             for (int L = K; L >= 1; --L) {
                 const float ax = cfk::lo(sw.acc[L]), ay = cfk::hi(sw.acc[L]);
-                if (sw.out_lane && (ax != ax || (sw.out_h[1] && ay != ay))) bad = p.iter_base + L;
+                if ((sw.outc[0] || sw.outc[C - 1]) && (ax != ax || (sw.out_h[1] && ay != ay)))
+                    bad = p.iter_base + L;
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(kFull, bad, o));

@@ -64,11 +64,11 @@ def px32(n9):
     Tm, T0 = f32(Ht + Hc), f32(Hc + Hb)
     D = [fma32(2, fma32(2, l, Wm), n12u), fma32(2, fma32(2, b, Tm), n12u),
          fma32(2, fma32(2, r, W0), n12u), fma32(2, fma32(2, f, T0), n12u)]
-    K5, K6 = f32(c + e), f32(a + g)
-    D += [f32(fma32(4, f32(b + l), fma32(2, a, K5)) + n12u),
-          f32(fma32(4, f32(b + r), fma32(2, c, K6)) + n12u),
-          f32(fma32(4, f32(r + f), fma32(2, g, K5)) + n12u),
-          f32(fma32(4, f32(l + f), fma32(2, e, K6)) + n12u)]
+    K5, K6 = f32(f32(c + e) + n12u), f32(f32(a + g) + n12u)
+    D += [fma32(4, f32(b + l), fma32(2, a, K5)),
+          fma32(4, f32(b + r), fma32(2, c, K6)),
+          fma32(4, f32(r + f), fma32(2, g, K5)),
+          fma32(4, f32(l + f), fma32(2, e, K6))]
     pick = lambda lft, rgt: rgt if abs(rgt) < abs(lft) else lft  # noqa: E731
     best = pick(pick(pick(D[0], D[1]), pick(D[2], D[3])), pick(pick(D[4], D[5]), pick(D[6], D[7])))
     return D, n12u, best
