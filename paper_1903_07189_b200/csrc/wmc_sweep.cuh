@@ -99,6 +99,10 @@ __host__ __device__ constexpr int smem_bytes_per_warp() {
 #ifndef CF_SCALAR
 // Packed fp32 pairs in one 64-bit register pair (PTX .b64) and sm_100
 // add/mul/fma.rn.f32x2 (SASS FADD2/FMUL2/FFMA2).
+// CAUTION (measured, ptxas 12.9): a mul.rn.f32x2 whose only use is an
+// add.rn.f32x2 IS contracted into FFMA2 despite .rn and --fmad=false, which
+// changes the rounding.  Every packed product here is either multi-use
+// (n12u) or a multiplicand of an explicit fma (H^w); keep it that way.
 using f2 = unsigned long long;
 __device__ __forceinline__ f2 add2(f2 a, f2 b) {
     f2 d;
