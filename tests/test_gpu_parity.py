@@ -153,3 +153,16 @@ def test_cpp_cli_matches_oracle():
     out = json.loads(subprocess.run([exe, "op", "--size", str(H), str(W), "--seed", "3"],
                                     capture_output=True, text=True, check=True).stdout)
     assert out["fnv1a"] == fnv(oracle.wmc_map_f32(img))
+
+
+@pytest.mark.parametrize("scale", [1e-38, 1e-30, 255.0, 1e6])
+def test_scaled_and_subnormal_inputs(scale):
+    """Parity holds at any intensity scale, incl. subnormal-range values
+    (packed f32x2 ops keep subnormals like the scalar oracle)."""
+    img = (cf.synth_image(37, 150, seed=17, n_rects=4, n_discs=4, sigma=0.1) *
+           np.float32(scale)).astype(np.float32)
+    d = torch.from_numpy(img).cuda()
+    assert_bitexact(cf.wmc_half_laplace(d).cpu().numpy(), oracle.wmc_map_f32(img), "map scaled")
+    got = cf.mc_flow(d, cf.FlowConfig(iters=7)).cpu().numpy()
+    ref, _ = oracle.flow_f32(img, 7, 1.0)
+    assert_bitexact(got, ref, f"flow scale={scale}")
