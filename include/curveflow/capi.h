@@ -122,6 +122,26 @@ CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t sr
                                   float dt, int32_t iter_base, int32_t* d_flag, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* 8-bit interleaved images (SPEC.md:62-69 per-channel processing, :79     */
+/* widen on load / clamp + round at save).  channels = 1 or 3 (else        */
+/* CF_EINVAL); in/out are HWC u8 with row pitch in BYTES;      */
+/* planes are planar fp32 on [0,1].                                        */
+/*   load: v = (float)q / 255.0f;  save: q = rint(fl(clamp(v,0,1) * 255)) */
+/* ---------------------------------------------------------------------- */
+CF_API int cf_image8_to_planes_f32(const uint8_t* in, int64_t in_pitch, int32_t w, int32_t h,
+                                   int32_t channels, float* planes, int64_t pitch,
+                                   int64_t plane_stride, void* stream);
+CF_API int cf_planes_f32_to_image8(const float* planes, int64_t pitch, int64_t plane_stride,
+                                   int32_t w, int32_t h, int32_t channels, uint8_t* out,
+                                   int64_t out_pitch, void* stream);
+/* mc_flow on an interleaved 8-bit image, per channel, result re-quantised. */
+CF_API size_t cf_wmc_filter_image8_workspace_bytes(int32_t w, int32_t h, int32_t channels);
+CF_API int cf_wmc_filter_image8(const uint8_t* in, int64_t in_pitch, uint8_t* out,
+                                int64_t out_pitch, int32_t w, int32_t h, int32_t channels,
+                                int32_t iters, float dt, void* workspace, size_t workspace_bytes,
+                                int32_t* first_bad_iter, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* Seeded synthetic image generator (BASELINE.json configs). */
 /* HOST memory, deterministic for a given (seed, params) on any thread     */
 /* count: linear ramp background, n_rects axis-aligned rectangles then     */

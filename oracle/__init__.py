@@ -38,6 +38,8 @@ def lib():
         L.or_flow_f32.argtypes = [_vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32, _i32, _pi32]
         L.or_flow_f64.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32, _pi32]
         L.or_u8_to_f32.argtypes = [_vp, _vp, _i64]
+        L.or_quantize_u8.argtypes = [_vp, _vp, _i64]
+        L.or_quantize_u8.restype = None
         L.or_wmc_naive_f64.argtypes = [_vp, _vp, _i32, _i32]
         L.or_kernel_bank_numerators.argtypes = [_pi32]
         for f in ("or_wmc_map_f64", "or_wmc_map_f32", "or_flow_f32", "or_flow_f64"):
@@ -166,3 +168,21 @@ def kernel_bank_x12():
     buf = (C.c_int32 * 72)()
     lib().or_kernel_bank_numerators(buf)
     return np.array(list(buf), dtype=np.int32).reshape(8, 3, 3)
+
+
+def quantize_u8(v):
+    """Save-time quantisation: rint(clamp(v, 0, 1) * 255)."""
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    out = np.empty(v.shape, dtype=np.uint8)
+    lib().or_quantize_u8(v.ctypes.data, out.ctypes.data, v.size)
+    return out
+
+
+def flow_image8(img8, iters, dt=1.0, threads=None):
+    """Reference for mc_flow on an interleaved 8-bit image (H,W) / (H,W,3)."""
+    a = np.asarray(img8, dtype=np.uint8)
+    planes = a[None] if a.ndim == 2 else np.ascontiguousarray(np.moveaxis(a, 2, 0))
+    f = u8_to_f32(planes)
+    out, bad = flow_f32(f, iters, dt, threads)
+    q = quantize_u8(out)
+    return (q[0] if a.ndim == 2 else np.ascontiguousarray(np.moveaxis(q, 0, 2))), bad

@@ -232,6 +232,15 @@ OR_EXPORT int or_flow_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32
     return rc;
 }
 
+/* Save-time quantisation: clamp to [0,1] (NaN -> 0), scale by
+ * 255 in fp32, round half to even. */
+OR_EXPORT void or_quantize_u8(const float* in, uint8_t* out, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) {
+        const float c = fminf(fmaxf(in[i], 0.0f), 1.0f);
+        out[i] = (uint8_t)rintf(c * 255.0f);
+    }
+}
+
 /* 8-bit widening on load: q / 255 in IEEE fp32. */
 OR_EXPORT void or_u8_to_f32(const uint8_t* in, float* out, int64_t n) {
     for (int64_t i = 0; i < n; ++i) out[i] = (float)in[i] / 255.0f;

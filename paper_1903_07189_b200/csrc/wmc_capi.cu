@@ -180,6 +180,9 @@ __global__ void u8_to_f32_kernel(const uint8_t* in, int64_t in_pitch, int64_t in
 
 }  // namespace
 
+// Shared with wmc_io.cu; hidden (not part of the C-ABI).
+extern "C" void cf_internal_set_cuda_error(int e) { g_last_cuda = e; }
+
 extern "C" {
 
 CF_API const char* cf_version(void) { return "curveflow-b200 0.1.0 (sm_100a)"; }

@@ -32,6 +32,7 @@ from ._lib import CF_ENONFINITE, check, lib
 __all__ = [
     "FlowConfig", "FlowError", "wmc_half_laplace", "mc_flow", "mc_flow_u8", "kernel",
     "kernel_bank", "split_channels", "merge_channels", "synth_image", "sweeps_band",
+    "mc_flow_image8",
     "max_sweeps_per_launch", "workspace_bytes",
 ]
 
@@ -194,6 +195,39 @@ def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=
     if host:
         return res.cpu().numpy() if isinstance(img_u8, np.ndarray) else res.cpu()
     return res
+
+
+def mc_flow_image8(img, cfg: FlowConfig, *, check_finite: bool = True):
+    """mc_flow on an interleaved 8-bit image (H, W) or (H, W, 3): widened on
+    load (q/255), filtered per channel, clamped and rounded back to uint8 at
+    save time.  numpy in -> numpy out; torch CUDA uint8
+    in -> torch CUDA uint8 out."""
+    torch = _torch()
+    cfg.validate()
+    host = isinstance(img, np.ndarray)
+    src = torch.from_numpy(np.ascontiguousarray(img, dtype=np.uint8)).cuda() if host else \
+        img.contiguous()
+    if src.dtype != torch.uint8:
+        raise TypeError("mc_flow_image8 expects uint8 input")
+    if src.dim() == 2:
+        H, W, ch = src.shape[0], src.shape[1], 1
+    elif src.dim() == 3 and src.shape[2] == 3:
+        H, W, ch = src.shape[0], src.shape[1], 3
+    else:
+        raise ValueError("unsupported channel count (SPEC.md:65): expected 1 or 3")
+    out = torch.empty_like(src)
+    nbytes = int(lib().cf_wmc_filter_image8_workspace_bytes(W, H, ch))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=src.device)
+    bad = C.c_int32(0)
+    with torch.cuda.device(src.device):
+        rc = lib().cf_wmc_filter_image8(src.data_ptr(), W * ch, out.data_ptr(), W * ch, W, H, ch,
+                                        int(cfg.iters), float(cfg.dt), ws.data_ptr(), nbytes,
+                                        C.byref(bad) if check_finite else None,
+                                        _stream_ptr(torch, src.device))
+    if rc == CF_ENONFINITE:
+        raise FlowError(bad.value)
+    check(rc, "mc_flow_image8")
+    return out.cpu().numpy() if host else out
 
 
 def max_sweeps_per_launch() -> int:

@@ -166,3 +166,18 @@ def test_scaled_and_subnormal_inputs(scale):
     got = cf.mc_flow(d, cf.FlowConfig(iters=7)).cpu().numpy()
     ref, _ = oracle.flow_f32(img, 7, 1.0)
     assert_bitexact(got, ref, f"flow scale={scale}")
+
+
+@pytest.mark.parametrize("ch", [1, 3])
+def test_flow_image8_interleaved(ch):
+    """Interleaved 8-bit in/out == oracle widen/flow/quantise."""
+    planes = [cf.synth_image(41, 67, seed=10 + c, n_rects=4, n_discs=4, sigma=0.1, dtype="u8")
+              for c in range(ch)]
+    img = planes[0] if ch == 1 else np.stack(planes, axis=2)
+    for iters in (0, 1, 6):
+        got = cf.mc_flow_image8(img, cf.FlowConfig(iters=iters))
+        ref, _ = oracle.flow_image8(img, iters, 1.0)
+        assert got.dtype == np.uint8 and got.shape == img.shape
+        assert np.array_equal(got, ref), f"ch={ch} iters={iters}"
+    with pytest.raises(ValueError):
+        cf.mc_flow_image8(np.zeros((4, 4, 2), np.uint8), cf.FlowConfig(iters=1))

@@ -292,3 +292,15 @@ def test_u8_widening():
     """8-bit inputs widened on load, q/255 in IEEE fp32."""
     q = np.arange(256, dtype=np.uint8)
     assert np.array_equal(oracle.u8_to_f32(q), q.astype(np.float32) / np.float32(255.0))
+
+
+def test_quantize_u8():
+    """SPEC.md:79 save-time clamp + round (half to even), NaN -> 0."""
+    v = np.array([-1.0, 0.0, 0.5 / 255, 1.5 / 255, 2.5 / 255, 0.5, 1.0, 2.0, np.nan, np.inf],
+                 np.float32)
+    q = oracle.quantize_u8(v)
+    ref = np.rint(np.clip(np.nan_to_num(v, nan=0.0), 0, 1).astype(np.float32) * np.float32(255))
+    assert np.array_equal(q, ref.astype(np.uint8))
+    # round trip of every 8-bit value
+    allq = np.arange(256, dtype=np.uint8)
+    assert np.array_equal(oracle.quantize_u8(oracle.u8_to_f32(allq)), allq)
