@@ -102,6 +102,19 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
                                 size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* solve_l2_area, A = identity (Eq. 30 with      */
+/* -dR_area/dU ~ H^w): u <- f, then iters explicit steps                   */
+/*   U' = U + dt * ((f - U) + lambda * wmc(U))                             */
+/* with wmc the flow's canonical fp32 H^w.  f and u are    */
+/* distinct device images of the same geometry; dt > 0, lambda >= 0.        */
+/* Workspace / non-finite reporting as cf_wmc_filter_f32.                   */
+/* ---------------------------------------------------------------------- */
+CF_API int cf_wmc_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t h,
+                                    int64_t pitch, int32_t planes, int64_t plane_stride,
+                                    int32_t iters, float dt, float lambda, void* workspace,
+                                    size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* Row-band primitive for sharded filtering (BASELINE cfg 4).               */
 /* Runs `sweeps` (1 <= sweeps <= cf_wmc_max_sweeps_per_launch()) Jacobi     */
 /* sweeps of the flow in ONE launch, producing global rows [y0, y1) of the  */

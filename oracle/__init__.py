@@ -40,6 +40,9 @@ def lib():
         L.or_u8_to_f32.argtypes = [_vp, _vp, _i64]
         L.or_quantize_u8.argtypes = [_vp, _vp, _i64]
         L.or_quantize_u8.restype = None
+        L.or_solve_l2_area_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32,
+                                           _f32, _i32, _pi32]
+        L.or_solve_l2_area_f32.restype = C.c_int
         L.or_wmc_naive_f64.argtypes = [_vp, _vp, _i32, _i32]
         L.or_kernel_bank_numerators.argtypes = [_pi32]
         for f in ("or_wmc_map_f64", "or_wmc_map_f32", "or_flow_f32", "or_flow_f64"):
@@ -186,3 +189,16 @@ def flow_image8(img8, iters, dt=1.0, threads=None):
     out, bad = flow_f32(f, iters, dt, threads)
     q = quantize_u8(out)
     return (q[0] if a.ndim == 2 else np.ascontiguousarray(np.moveaxis(q, 0, 2))), bad
+
+
+def solve_l2_area_f32(f, iters, dt, lam, threads=None):
+    """fp32 canonical solve_l2_area (A = I); returns (U^iters, bad_iter)."""
+    a = np.ascontiguousarray(f, dtype=np.float32)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    u = np.empty_like(a3)
+    bad = C.c_int32(0)
+    rc = lib().or_solve_l2_area_f32(a3.ctypes.data, u.ctypes.data, w, h, w, P, h * w, int(iters),
+                                    float(dt), float(lam), _threads(threads), C.byref(bad))
+    assert rc in (0, 3), rc
+    return (u[0] if a.ndim == 2 else u), bad.value

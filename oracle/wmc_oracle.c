@@ -232,6 +232,63 @@ OR_EXPORT int or_flow_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32
     return rc;
 }
 
+/* solve_l2_area with A = I: U^0 = f, then iters Jacobi
+ * steps U' = fmaf(dt, fmaf(lambda, H^w(U), fmaf(U, -1, f)), U), H^w the
+ * flow's canonical fp32 map.  u receives U^iters; 3 + *bad_iter on a
+ * non-finite iterate. */
+typedef struct {
+    const float* in;
+    const float* f;
+    float* out;
+    int w, h;
+    int64_t pitch;
+    float dt, lambda;
+    volatile int* bad;
+} l2_ctx;
+
+static void l2_row(void* vctx, int y) {
+    l2_ctx* c = (l2_ctx*)vctx;
+    int bad = 0;
+    for (int x = 0; x < c->w; ++x) {
+        const int64_t i = (int64_t)y * c->pitch + x;
+        const float hw = wmc_at_f32(c->in, c->w, c->h, c->pitch, y, x, 0, NULL);
+        const float r = fmaf(c->in[i], -1.0f, c->f[i]);
+        const float v = fmaf(c->dt, fmaf(c->lambda, hw, r), c->in[i]);
+        if (!isfinite(v)) bad = 1;
+        c->out[i] = v;
+    }
+    if (bad) c->bad[y] = 1;
+}
+
+OR_EXPORT int or_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t h, int64_t pitch,
+                                   int32_t planes, int64_t plane_stride, int32_t iters, float dt,
+                                   float lambda, int32_t threads, int32_t* bad_iter) {
+    if (w <= 0 || h <= 0 || planes <= 0 || iters < 0 || pitch < w) return 1;
+    if (bad_iter) *bad_iter = 0;
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)pitch * (size_t)h);
+    int* bad = (int*)calloc((size_t)h, sizeof(int));
+    int rc = 0;
+    for (int p = 0; p < planes && rc == 0; ++p) {
+        float* U = u + p * plane_stride;
+        const float* F = f + p * plane_stride;
+        memcpy(U, F, sizeof(float) * (size_t)pitch * (size_t)h);
+        float *A = U, *B = tmp;
+        for (int t = 1; t <= iters; ++t) {
+            memset(bad, 0, sizeof(int) * (size_t)h);
+            l2_ctx c = {A, F, B, w, h, pitch, dt, lambda, bad};
+            for_rows(h, threads, l2_row, &c);
+            float* s = A; A = B; B = s;
+            int any = 0;
+            for (int y = 0; y < h; ++y) any |= bad[y];
+            if (any) { if (bad_iter) *bad_iter = t; rc = 3; break; }
+        }
+        if (A != U) memcpy(U, A, sizeof(float) * (size_t)pitch * (size_t)h);
+    }
+    free(tmp);
+    free(bad);
+    return rc;
+}
+
 /* Save-time quantisation: clamp to [0,1] (NaN -> 0), scale by
  * 255 in fp32, round half to even. */
 OR_EXPORT void or_quantize_u8(const float* in, uint8_t* out, int64_t n) {

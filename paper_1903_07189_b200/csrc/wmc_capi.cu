@@ -67,16 +67,16 @@ constexpr size_t smem_bytes() {
     return (size_t)cfk::kWarpsPerBlock * cfk::smem_bytes_per_warp<K>();
 }
 
-template <int K, bool MAP>
+template <int K, int MODE>
 int kernel_occupancy_warps() {
     static int cached = -1;  // per instantiation; identical on every B200
     if (cached < 0) {
         if (smem_bytes<K>() > 48 * 1024)
-            cudaFuncSetAttribute(cfk::wmc_sweeps_kernel<K, MAP>,
+            cudaFuncSetAttribute(cfk::wmc_sweeps_kernel<K, MODE>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<K>());
         int blocks = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks, cfk::wmc_sweeps_kernel<K, MAP>, cfk::kThreads,
+                &blocks, cfk::wmc_sweeps_kernel<K, MODE>, cfk::kThreads,
                 smem_bytes<K>()) !=
                 cudaSuccess ||
             blocks <= 0)
@@ -108,29 +108,29 @@ void plan_strips(cfk::SweepParams& p, int K, int slots) {
     p.n_strips = (rows + p.strip_rows - 1) / p.strip_rows;
 }
 
-template <int K, bool MAP>
+template <int K, int MODE>
 int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
     using G = cfk::Geo<K>;
     p.n_chunks = (p.w + G::S - 1) / G::S;
-    plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MAP>());
+    plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MODE>());
     const int64_t tasks = (int64_t)((p.n_chunks + 1) / 2) * p.n_strips * p.planes;
     const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
     if (blocks > INT_MAX) return CF_EINVAL;
-    cfk::wmc_sweeps_kernel<K, MAP><<<(unsigned)blocks, cfk::kThreads, smem_bytes<K>(), s>>>(p);
+    cfk::wmc_sweeps_kernel<K, MODE><<<(unsigned)blocks, cfk::kThreads, smem_bytes<K>(), s>>>(p);
     CF_CUDA(cudaGetLastError());
     return CF_OK;
 }
 
-template <bool MAP>
+template <int MODE>
 int launch(const cfk::SweepParams& p, int K, const DevInfo& d, cudaStream_t s) {
-    if constexpr (MAP) {
-        return launch_k<1, true>(p, d, s);
+    if constexpr (MODE == cfk::kModeMap) {
+        return launch_k<1, MODE>(p, d, s);
     } else {
         switch (K) {
-            case 1: return launch_k<1, false>(p, d, s);
-            case 2: return launch_k<2, false>(p, d, s);
-            case 3: return launch_k<3, false>(p, d, s);
-            case 4: return launch_k<4, false>(p, d, s);
+            case 1: return launch_k<1, MODE>(p, d, s);
+            case 2: return launch_k<2, MODE>(p, d, s);
+            case 3: return launch_k<3, MODE>(p, d, s);
+            case 4: return launch_k<4, MODE>(p, d, s);
             default: return CF_EINVAL;
         }
     }
@@ -234,7 +234,7 @@ CF_API int cf_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int
     p.src_row0 = p.dst_row0 = 0;
     p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
     p.dt = 0.f; p.iter_base = 0; p.flag = nullptr;
-    return launch<true>(p, 1, d, (cudaStream_t)stream);
+    return launch<cfk::kModeMap>(p, 1, d, (cudaStream_t)stream);
 }
 
 CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch, int32_t planes,
@@ -244,10 +244,15 @@ CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch,
     return kWsHeader + (size_t)elems * sizeof(float);
 }
 
+struct DataTerm {            // solve_l2_area: U' = U + dt*((f - U) + lambda*H^w)
+    const float* f = nullptr;
+    float lambda = 0.0f;
+};
+
 static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t src_plane,
                     float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
                     int64_t plane_stride, int32_t iters, float dt, void* workspace,
-                    int32_t* first_bad_iter, cudaStream_t s) {
+                    int32_t* first_bad_iter, cudaStream_t s, DataTerm dterm = {}) {
     DevInfo d;
     if (int rc = device_info(&d)) return rc;
     int32_t* flag = reinterpret_cast<int32_t*>(workspace);
@@ -277,7 +282,10 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
         p.src_row0 = p.dst_row0 = 0;
         p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
         p.dt = dt; p.iter_base = iter; p.flag = flag;
-        if (int rc = launch<false>(p, ks[i], d, s)) return rc;
+        p.fdata = dterm.f; p.f_pitch = pitch; p.f_plane = plane_stride; p.lambda = dterm.lambda;
+        const int rc = dterm.f ? launch<cfk::kModeL2>(p, ks[i], d, s)
+                               : launch<cfk::kModeFlow>(p, ks[i], d, s);
+        if (rc) return rc;
         iter += ks[i];
         std::swap(cur, nxt);
     }
@@ -329,6 +337,30 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
                     iters, dt, workspace, first_bad_iter, s);
 }
 
+CF_API int cf_wmc_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t h,
+                                    int64_t pitch, int32_t planes, int64_t plane_stride,
+                                    int32_t iters, float dt, float lambda, void* workspace,
+                                    size_t workspace_bytes, int32_t* first_bad_iter, void* stream) {
+    if (!f || !u || f == u || !shape_ok(w, h, pitch, planes, plane_stride) || iters < 0)
+        return CF_EINVAL;
+    if (!(dt > 0.0f) || !(dt < 3.0e38f) || !(lambda >= 0.0f) || !(lambda < 3.0e38f))
+        return CF_EINVAL;
+    if (first_bad_iter) *first_bad_iter = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int pl = 0; pl < planes; ++pl)  // U^0 = f
+        CF_CUDA(cudaMemcpy2DAsync(u + pl * plane_stride, pitch * 4, f + pl * plane_stride,
+                                  pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
+    if (iters == 0) return CF_OK;
+    if (!workspace ||
+        workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))
+        return CF_EINVAL;
+    DataTerm dterm;
+    dterm.f = f;
+    dterm.lambda = lambda;
+    return run_flow(u, false, pitch, plane_stride, u, w, h, pitch, planes, plane_stride, iters,
+                    dt, workspace, first_bad_iter, s, dterm);
+}
+
 CF_API int cf_wmc_filter_query_nonfinite(const void* workspace, int32_t* first_bad_iter,
                                          void* stream) {
     if (!workspace || !first_bad_iter) return CF_EINVAL;
@@ -362,7 +394,7 @@ CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t sr
     p.src_row0 = src_row0; p.dst_row0 = dst_row0;
     p.w = w; p.h = h; p.y0 = y0; p.y1 = y1; p.planes = 1;
     p.dt = dt; p.iter_base = iter_base; p.flag = d_flag;
-    return launch<false>(p, sweeps, d, (cudaStream_t)stream);
+    return launch<cfk::kModeFlow>(p, sweeps, d, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -76,7 +76,16 @@ struct SweepParams {
     float dt;
     int32_t iter_base;
     int32_t* flag;            // nullable
+    // MODE == kModeL2 (solve_l2_area): data term f and lambda
+    const float* fdata;       // global row 0 of plane 0 (same column geometry as src)
+    int64_t f_pitch, f_plane; // elements
+    float lambda;
 };
+
+// Per-pixel update a launch applies at every level.
+constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_flow)
+constexpr int kModeMap = 1;   // out = H^w(U), one level, fp64 near-tie rule (wmc_half_laplace)
+constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)
 
 // Column geometry for K levels: each chunk window overlaps its neighbours by
 // A = K columns per side (the trapezoid shrinks one column per level).
@@ -280,9 +289,10 @@ __device__ __noinline__ float wmc_px_f64(float a, float b, float c, float l, flo
 }
 
 // ---------------------------------------------------------------------------
-template <int K, bool MAP>
+template <int K, int MODE>
 struct SweepWarp {
     using G = Geo<K>;
+    static constexpr bool MAP = MODE == kModeMap;
 
     const SweepParams& P;
     int lane;
@@ -296,6 +306,7 @@ struct SweepWarp {
     __device__ __forceinline__ int rhi(int L) const { return min(ye + (K - L), P.h); }
     const float* srcp;            // plane base
     float* dstp;                  // plane base
+    const float* fp;              // plane base of f (kModeL2)
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     f2 acc[K + 1];
     f2 hc[K + 1][C], tm[K + 1][C];  // carried row sums per level and pixel pair
@@ -427,6 +438,19 @@ struct SweepWarp {
                     hw = pk(h0, h1);
                 }
                 nv[j - 1] = hw;
+            } else if constexpr (MODE == kModeL2) {
+                // SPEC.md:298 with A = I: U' = U + dt*((f - U) + lambda*H^w(U))
+                const float* frow = fp + (int64_t)y * P.f_pitch;
+                int x0 = xf[0] + j - 1, x1 = xf[1] + j - 1;
+                if (CHECKED) {
+                    x0 = min(max(x0, 0), P.w - 1);
+                    x1 = min(max(x1, 0), P.w - 1);
+                }
+                const f2 fv = pk(__ldg(frow + x0), __ldg(frow + x1));
+                const f2 r = fma2(o[j], splat(-1.0f), fv);         // f - u
+                const f2 sdir = fma2(splat(P.lambda), hw, r);      // (f-u) + lambda*H
+                nv[j - 1] = fma2(splat(P.dt), sdir, o[j]);
+                if (outc[j - 1]) acc[L] = fma2(nv[j - 1], kZero2, acc[L]);
             } else {
                 nv[j - 1] = fma2(splat(P.dt), hw, o[j]);   // u + dt * H^w
                 if (outc[j - 1]) acc[L] = fma2(nv[j - 1], kZero2, acc[L]);
@@ -567,8 +591,9 @@ struct SweepWarp {
     }
 };
 
-template <int K, bool MAP>
+template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const SweepParams p) {
+    constexpr bool MAP = MODE == kModeMap;
     using G = Geo<K>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -580,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const Swe
     const int strip = rest % p.n_strips;
     const int plane = rest / p.n_strips;
 
-    SweepWarp<K, MAP> sw(p);
+    SweepWarp<K, MODE> sw(p);
     sw.lane = threadIdx.x & 31;
 #pragma unroll
     for (int j = 0; j < C; ++j) {
@@ -602,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const Swe
     if (sw.ys >= sw.ye) return;
     sw.srcp = p.src + (int64_t)plane * p.src_plane;
     sw.dstp = p.dst + (int64_t)plane * p.dst_plane;
+    sw.fp = MODE == kModeL2 ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K>();
 

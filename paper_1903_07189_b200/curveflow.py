@@ -32,7 +32,7 @@ from ._lib import CF_ENONFINITE, check, lib
 __all__ = [
     "FlowConfig", "FlowError", "wmc_half_laplace", "mc_flow", "mc_flow_u8", "kernel",
     "kernel_bank", "split_channels", "merge_channels", "synth_image", "sweeps_band",
-    "mc_flow_image8",
+    "mc_flow_image8", "SolverConfig", "SolveReport", "solve_l2_area",
     "max_sweeps_per_launch", "workspace_bytes",
 ]
 
@@ -228,6 +228,65 @@ def mc_flow_image8(img, cfg: FlowConfig, *, check_finite: bool = True):
         raise FlowError(bad.value)
     check(rc, "mc_flow_image8")
     return out.cpu().numpy() if host else out
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """SPEC.md:286-289 (the fields the l2_area model uses; operator A = identity)."""
+
+    lam: float = 0.0
+    dt: float = 0.15
+    iters: int = 500
+    model: str = "l2_area"
+
+    def validate(self) -> None:
+        if self.model != "l2_area":
+            raise NotImplementedError("only model='l2_area' (SPEC.md:296) is built on the "
+                                      "B200 path; l1_area / l2_epstv are out of scope this round")
+        if not (self.dt > 0.0) or not np.isfinite(self.dt):
+            raise ValueError("SolverConfig.dt must be > 0")
+        if not (self.lam >= 0.0) or not np.isfinite(self.lam):
+            raise ValueError("SolverConfig.lam must be >= 0")
+        if int(self.iters) != self.iters or self.iters < 0:
+            raise ValueError("SolverConfig.iters must be a nonnegative integer")
+
+
+@dataclass
+class SolveReport:
+    """SPEC.md:290-293 subset: the final image, iterations run, and the final
+    data fidelity 0.5*||U - f||^2 (double)."""
+
+    image: object
+    iters: int
+    fidelity: float
+
+
+def solve_l2_area(f, cfg: SolverConfig) -> SolveReport:
+    """solve_l2_area (SPEC.md:296-303, A = I): U^0 = f,
+    U <- U + dt*((f - U) + lam*H^w(U)); raises FlowError(iteration) on a
+    non-finite iterate."""
+    torch = _torch()
+    cfg.validate()
+    src, host = _device_image(f)
+    f3, squeeze = _as_planes(src.contiguous())
+    P, H, W = f3.shape
+    u = torch.empty_like(f3)
+    nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=f3.device)
+    bad = C.c_int32(0)
+    with torch.cuda.device(f3.device):
+        rc = lib().cf_wmc_solve_l2_area_f32(f3.data_ptr(), u.data_ptr(), W, H, W, P, H * W,
+                                            int(cfg.iters), float(cfg.dt), float(cfg.lam),
+                                            ws.data_ptr(), nbytes, C.byref(bad),
+                                            _stream_ptr(torch, f3.device))
+    if rc == CF_ENONFINITE:
+        raise FlowError(bad.value)
+    check(rc, "solve_l2_area")
+    fid = float(0.5 * ((u.double() - f3.double()) ** 2).sum().item())
+    res = u[0] if squeeze else u
+    if host:
+        res = res.cpu().numpy() if isinstance(f, np.ndarray) else res.cpu()
+    return SolveReport(image=res, iters=int(cfg.iters), fidelity=fid)
 
 
 def max_sweeps_per_launch() -> int:

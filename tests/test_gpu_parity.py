@@ -181,3 +181,17 @@ def test_flow_image8_interleaved(ch):
         assert np.array_equal(got, ref), f"ch={ch} iters={iters}"
     with pytest.raises(ValueError):
         cf.mc_flow_image8(np.zeros((4, 4, 2), np.uint8), cf.FlowConfig(iters=1))
+
+
+@pytest.mark.parametrize("lam,dt,iters", [(0.0, 0.15, 9), (3.0, 0.15, 1), (3.0, 0.15, 20),
+                                          (20.0, 0.05, 37), (150.0, 0.002, 10)])
+def test_solve_l2_area_bitexact(lam, dt, iters):
+    f = np.stack([cf.synth_image(53, 140, seed=40 + s, n_rects=5, n_discs=5, sigma=0.1)
+                  for s in range(2)])
+    rep = cf.solve_l2_area(torch.from_numpy(f).cuda(), cf.SolverConfig(lam=lam, dt=dt,
+                                                                        iters=iters))
+    ref, bad = oracle.solve_l2_area_f32(f, iters, dt, lam)
+    assert bad == 0
+    assert_bitexact(rep.image.cpu().numpy(), ref, f"l2 lam={lam} iters={iters}")
+    if lam == 0.0:
+        assert_bitexact(rep.image.cpu().numpy(), f, "lambda=0 fixed point")

@@ -304,3 +304,27 @@ def test_quantize_u8():
     # round trip of every 8-bit value
     allq = np.arange(256, dtype=np.uint8)
     assert np.array_equal(oracle.quantize_u8(oracle.u8_to_f32(allq)), allq)
+
+
+# ------------------------------------------------------- solve_l2_area -----
+def test_l2_area_lambda0_is_fixed_point():
+    """lambda = 0, A = I -> f unchanged, bitwise."""
+    f = cf.synth_image(23, 31, seed=5, n_rects=3, n_discs=3, sigma=0.1)
+    u, bad = oracle.solve_l2_area_f32(f, 25, 0.15, 0.0)
+    assert bad == 0 and np.array_equal(u.view(np.uint32), f.view(np.uint32))
+
+
+def test_l2_area_homogeneity():
+    """SPEC.md:331: step(aU, af) = a*step(U, f) (exact for a = 2)."""
+    f = cf.synth_image(19, 27, seed=6, n_rects=3, n_discs=3, sigma=0.1)
+    u1, _ = oracle.solve_l2_area_f32(f, 10, 0.15, 3.0)
+    u2, _ = oracle.solve_l2_area_f32(2 * f, 10, 0.15, 3.0)
+    assert np.array_equal((2 * u1).view(np.uint32), u2.view(np.uint32))
+
+
+def test_l2_area_smooths_toward_data():
+    f = cf.synth_image(40, 40, seed=7, n_rects=3, n_discs=3, sigma=0.1)
+    u, _ = oracle.solve_l2_area_f32(f, 200, 0.15, 5.0)
+    # fixed point of U = f + lam*H^w(U): smoother than f (noise variance down)
+    lap = lambda a: a[1:-1, 1:-1] - 0.25 * (a[:-2, 1:-1] + a[2:, 1:-1] + a[1:-1, :-2] + a[1:-1, 2:])  # noqa: E731
+    assert lap(u).var() < 0.5 * lap(f).var()
