@@ -155,6 +155,25 @@ CF_API int cf_wmc_filter_image8(const uint8_t* in, int64_t in_pitch, uint8_t* ou
                                 int32_t* first_bad_iter, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* Reductions over the WMC map.    */
+/* energy: *d_out (device double) = sum |H^w|^q, q > 0, in the fixed order */
+/*   of csrc/wmc_reduce.cu (32-column butterfly blocks, blocks in x order, */
+/*   rows in y order, planes in order) -- deterministic, bit-exact for     */
+/*   q in {0.5, 1, 2}.                                                     */
+/* histogram: d_counts[nbins] (device u64) of floor((H^w*scale - lo)/width) */
+/*   clamped to [0, nbins-1] (NaN -> bin 0); the reference's binning is    */
+/*   scale = 255 (0-255 intensities), lo = -256, width = 1, nbins = 512.   */
+/* ---------------------------------------------------------------------- */
+CF_API size_t cf_wmc_reduce_workspace_bytes(int32_t w, int32_t h, int32_t planes);
+CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pitch,
+                             int32_t planes, int64_t plane_stride, double q, double* d_out,
+                             void* workspace, size_t workspace_bytes, void* stream);
+CF_API int cf_wmc_histogram(const float* img, int32_t w, int32_t h, int64_t pitch,
+                            int32_t planes, int64_t plane_stride, float scale, float lo,
+                            float width, int32_t nbins, uint64_t* d_counts, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* Seeded synthetic image generator (BASELINE.json configs). */
 /* HOST memory, deterministic for a given (seed, params) on any thread     */
 /* count: linear ramp background, n_rects axis-aligned rectangles then     */

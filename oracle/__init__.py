@@ -43,6 +43,10 @@ def lib():
         L.or_solve_l2_area_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32,
                                            _f32, _i32, _pi32]
         L.or_solve_l2_area_f32.restype = C.c_int
+        L.or_energy_from_map.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32]
+        L.or_energy_from_map.restype = C.c_double
+        L.or_histogram_from_map.argtypes = [_vp, _i64, _f32, _f32, _f32, _i32, _vp]
+        L.or_histogram_from_map.restype = None
         L.or_wmc_naive_f64.argtypes = [_vp, _vp, _i32, _i32]
         L.or_kernel_bank_numerators.argtypes = [_pi32]
         for f in ("or_wmc_map_f64", "or_wmc_map_f32", "or_flow_f32", "or_flow_f64"):
@@ -202,3 +206,20 @@ def solve_l2_area_f32(f, iters, dt, lam, threads=None):
                                     float(dt), float(lam), _threads(threads), C.byref(bad))
     assert rc in (0, 3), rc
     return (u[0] if a.ndim == 2 else u), bad.value
+
+
+def wmc_energy(img, q=1.0, threads=None):
+    """Fixed-order energy sum |H^w|^q of the fp32 canonical map (tie rule)."""
+    m = np.ascontiguousarray(wmc_map_f32(img, threads), dtype=np.float32)
+    m3 = m[None] if m.ndim == 2 else m
+    P, h, w = m3.shape
+    qk = 1 if q == 1.0 else (2 if q == 2.0 else (3 if q == 0.5 else 0))
+    return lib().or_energy_from_map(m3.ctypes.data, w, h, P, float(q), qk)
+
+
+def wmc_histogram(img, scale=255.0, lo=-256.0, width=1.0, nbins=512, threads=None):
+    m = np.ascontiguousarray(wmc_map_f32(img, threads), dtype=np.float32)
+    counts = np.zeros(nbins, dtype=np.int64)
+    lib().or_histogram_from_map(m.ctypes.data, m.size, float(scale), float(lo), float(width),
+                                int(nbins), counts.ctypes.data)
+    return counts

@@ -289,6 +289,50 @@ OR_EXPORT int or_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t 
     return rc;
 }
 
+/* Energy sum |H|^q over a dense map (planes x h x w) in the fixed order of
+ * paper_1903_07189_b200/csrc/wmc_reduce.cu: per row, 32-column blocks
+ * reduced by the xor butterfly (offsets 16,8,4,2,1; lane 0's value), blocks
+ * summed in x order, rows in y order, planes in order.  qkind: 1 -> |H|,
+ * 2 -> H*H, 3 -> sqrt|H|, 0 -> pow(|H|, q). */
+OR_EXPORT double or_energy_from_map(const float* map, int32_t w, int32_t h, int32_t planes,
+                                    double q, int32_t qkind) {
+    double total = 0.0;
+    for (int p = 0; p < planes; ++p)
+        for (int y = 0; y < h; ++y) {
+            const float* r = map + ((int64_t)p * h + y) * w;
+            double row = 0.0;
+            for (int x0 = 0; x0 < w; x0 += 32) {
+                double v[32];
+                for (int l = 0; l < 32; ++l) {
+                    const int x = x0 + l;
+                    if (x >= w) { v[l] = 0.0; continue; }
+                    const double a = fabs((double)r[x]);
+                    v[l] = qkind == 1 ? a : (qkind == 2 ? a * a : (qkind == 3 ? sqrt(a) : pow(a, q)));
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    double nv[32];
+                    for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ o];
+                    memcpy(v, nv, sizeof(v));
+                }
+                row = row + v[0];
+            }
+            total = total + row;
+        }
+    return total;
+}
+
+/* Histogram bins of a map: floor((v*scale - lo)/width) clamped (NaN -> 0). */
+OR_EXPORT void or_histogram_from_map(const float* map, int64_t n, float scale, float lo,
+                                     float width, int32_t nbins, int64_t* counts) {
+    memset(counts, 0, sizeof(int64_t) * (size_t)nbins);
+    for (int64_t i = 0; i < n; ++i) {
+        const float t = (map[i] * scale - lo) / width;
+        int b = (t != t) ? 0 : (int)floorf(fminf(fmaxf(t, -1.0f), (float)nbins));
+        b = b < 0 ? 0 : (b > nbins - 1 ? nbins - 1 : b);
+        counts[b]++;
+    }
+}
+
 /* Save-time quantisation: clamp to [0,1] (NaN -> 0), scale by
  * 255 in fp32, round half to even. */
 OR_EXPORT void or_quantize_u8(const float* in, uint8_t* out, int64_t n) {

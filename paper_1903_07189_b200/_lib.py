@@ -50,6 +50,10 @@ SIGNATURES = {
     "cf_wmc_filter_image8_workspace_bytes": (_sz, [_i32, _i32, _i32]),
     "cf_wmc_filter_image8": (C.c_int, [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _f32, _vp,
                                        _sz, _pi32, _vp]),
+    "cf_wmc_reduce_workspace_bytes": (_sz, [_i32, _i32, _i32]),
+    "cf_wmc_energy_f64": (C.c_int, [_vp, _i32, _i32, _i64, _i32, _i64, _f64, _vp, _vp, _sz, _vp]),
+    "cf_wmc_histogram": (C.c_int, [_vp, _i32, _i32, _i64, _i32, _i64, _f32, _f32, _f32, _i32,
+                                   _vp, _vp, _sz, _vp]),
     "cf_synth_f32": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_synth_u8": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_kernel_bank_x12": (None, [_pi32]),

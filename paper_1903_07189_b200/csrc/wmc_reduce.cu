@@ -1,0 +1,157 @@
+// paper_1903_07189_b200/csrc/wmc_reduce.cu -- reductions over the WMC map
+// (SURVEY.md §8f rank 2): the WMC regularisation energy and the WMC value
+// histogram.
+//
+// Reference semantics:
+//  * energy(img, kind = WMC, q) = sum over pixels of |H^w|^q with H^w from
+//    wmc_half_laplace, q > 0 (default 1); "parallel
+//    reduction allowed with fixed summation order per row then ordered row
+//    combine (deterministic)".
+//  * corpus_stats histograms wmc_half_laplace values with bins of width 1
+//    over [-256, 256]; counts are integers.
+//
+// Fixed order used here (and restated by the oracle, bit-exact):
+//  per plane, per row y: the row is cut into 32-column blocks; a block's
+//  terms |H|^q (fp64) are combined by the butterfly tree of a warp xor-
+//  shuffle reduction (offsets 16, 8, 4, 2, 1, lane order fixed); a row sum is
+//  the sequential sum of its block sums in x order; the plane's energy is the
+//  sequential sum of its row sums in y order, and planes add in plane order.
+//  q = 1 -> |H|, q = 2 -> H*H, q = 0.5 -> sqrt(|H|) (correctly rounded, so
+//  bit-exact); any other q uses pow() (documented 1e-12 relative tolerance).
+// The map itself is cf_wmc_map_f32 (fp32, fp64 near-tie rule).
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/curveflow/capi.h"
+
+extern "C" void cf_internal_set_cuda_error(int e);  // wmc_capi.cu (not exported)
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double term(float hw, double q, int qkind) {
+    const double a = fabs((double)hw);
+    switch (qkind) {
+        case 1: return a;
+        case 2: return __dmul_rn(a, a);
+        case 3: return __dsqrt_rn(a);
+        default: return pow(a, q);
+    }
+}
+
+// One warp per row: block sums by xor butterfly, sequential over blocks.
+__global__ void row_energy_kernel(const float* __restrict__ map, int32_t w, int32_t h,
+                                  int64_t pitch, int32_t planes, int64_t plane_stride, double q,
+                                  int qkind, double* __restrict__ row_sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= (int64_t)h * planes) return;
+    const int64_t p = row / h, y = row % h;
+    const float* r = map + p * plane_stride + y * pitch;
+    double acc = 0.0;
+    for (int x0 = 0; x0 < w; x0 += 32) {
+        const int x = x0 + lane;
+        double v = x < w ? term(r[x], q, qkind) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
+        acc = __dadd_rn(acc, v);  // every lane holds the same block sum
+    }
+    if (lane == 0) row_sums[row] = acc;
+}
+
+// Ordered combine of the row sums (one thread: h*planes sequential adds).
+__global__ void ordered_sum_kernel(const double* __restrict__ row_sums, int64_t n,
+                                   double* __restrict__ out) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, row_sums[i]);
+        *out = s;
+    }
+}
+
+__global__ void histogram_kernel(const float* __restrict__ map, int32_t w, int32_t h,
+                                 int64_t pitch, int32_t planes, int64_t plane_stride, float scale,
+                                 float lo, float width, int32_t nbins,
+                                 unsigned long long* __restrict__ counts) {
+    const int64_t n = (int64_t)w * h * planes;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / ((int64_t)w * h), rem = i % ((int64_t)w * h);
+        const float v = map[p * plane_stride + (rem / w) * pitch + rem % w];
+        // bin = floor((v*scale - lo) / width), out-of-range -> clamped ends
+        const float t = __fdiv_rn(__fsub_rn(__fmul_rn(v, scale), lo), width);
+        int b = (t != t) ? 0 : (int)floorf(fminf(fmaxf(t, -1.0f), (float)nbins));
+        b = min(max(b, 0), nbins - 1);
+        atomicAdd(counts + b, 1ull);
+    }
+}
+
+int fail() {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cf_internal_set_cuda_error((int)e);
+        return CF_ECUDA;
+    }
+    return CF_OK;
+}
+
+int qkind_of(double q) { return q == 1.0 ? 1 : (q == 2.0 ? 2 : (q == 0.5 ? 3 : 0)); }
+
+}  // namespace
+
+extern "C" {
+
+CF_API size_t cf_wmc_reduce_workspace_bytes(int32_t w, int32_t h, int32_t planes) {
+    if (w <= 0 || h <= 0 || planes <= 0) return 0;
+    const size_t map = (((size_t)w * h * planes * sizeof(float)) + 255) & ~(size_t)255;
+    return map + (size_t)h * planes * sizeof(double) + 256;
+}
+
+CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pitch,
+                             int32_t planes, int64_t plane_stride, double q, double* d_out,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+    if (!img || !d_out || !workspace || w <= 0 || h <= 0 || planes <= 0 || pitch < w)
+        return CF_EINVAL;
+    if (!(q > 0.0) || !(q < 1e300)) return CF_EINVAL;
+    if (workspace_bytes < cf_wmc_reduce_workspace_bytes(w, h, planes)) return CF_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    float* map = reinterpret_cast<float*>(workspace);
+    const size_t map_bytes = (((size_t)w * h * planes * sizeof(float)) + 255) & ~(size_t)255;
+    double* rows = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + map_bytes);
+    // dense copy of the map (pitch = w) so the layout is independent of the input's
+    for (int p = 0; p < planes; ++p) {
+        int rc = cf_wmc_map_f32(img + p * plane_stride, map + (int64_t)p * w * h, w, h, pitch, 1,
+                                (int64_t)w * h, stream);
+        if (rc) return rc;
+    }
+    const int64_t nrows = (int64_t)h * planes;
+    row_energy_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(
+        map, w, h, w, planes, (int64_t)w * h, q, qkind_of(q), rows);
+    ordered_sum_kernel<<<1, 32, 0, s>>>(rows, nrows, d_out);
+    return fail();
+}
+
+CF_API int cf_wmc_histogram(const float* img, int32_t w, int32_t h, int64_t pitch,
+                            int32_t planes, int64_t plane_stride, float scale, float lo,
+                            float width, int32_t nbins, uint64_t* d_counts, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    if (!img || !d_counts || !workspace || w <= 0 || h <= 0 || planes <= 0 || pitch < w)
+        return CF_EINVAL;
+    if (nbins <= 0 || !(width > 0.0f) || !(scale == scale) || !(lo == lo)) return CF_EINVAL;
+    if (workspace_bytes < cf_wmc_reduce_workspace_bytes(w, h, planes)) return CF_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    float* map = reinterpret_cast<float*>(workspace);
+    for (int p = 0; p < planes; ++p) {
+        int rc = cf_wmc_map_f32(img + p * plane_stride, map + (int64_t)p * w * h, w, h, pitch, 1,
+                                (int64_t)w * h, stream);
+        if (rc) return rc;
+    }
+    if (cudaMemsetAsync(d_counts, 0, sizeof(uint64_t) * nbins, s) != cudaSuccess) return fail();
+    histogram_kernel<<<1184, 256, 0, s>>>(map, w, h, w, planes, (int64_t)w * h, scale, lo, width,
+                                          nbins, reinterpret_cast<unsigned long long*>(d_counts));
+    return fail();
+}
+
+}  // extern "C"

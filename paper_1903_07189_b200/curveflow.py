@@ -32,7 +32,7 @@ from ._lib import CF_ENONFINITE, check, lib
 __all__ = [
     "FlowConfig", "FlowError", "wmc_half_laplace", "mc_flow", "mc_flow_u8", "kernel",
     "kernel_bank", "split_channels", "merge_channels", "synth_image", "sweeps_band",
-    "mc_flow_image8", "SolverConfig", "SolveReport", "solve_l2_area",
+    "mc_flow_image8", "wmc_energy", "wmc_histogram", "SolverConfig", "SolveReport", "solve_l2_area",
     "max_sweeps_per_launch", "workspace_bytes",
 ]
 
@@ -287,6 +287,42 @@ def solve_l2_area(f, cfg: SolverConfig) -> SolveReport:
     if host:
         res = res.cpu().numpy() if isinstance(f, np.ndarray) else res.cpu()
     return SolveReport(image=res, iters=int(cfg.iters), fidelity=fid)
+
+
+def wmc_energy(img, q: float = 1.0) -> float:
+    """WMC regularisation energy sum |H^w|^q, q > 0, with the
+    deterministic fixed-order reduction of SPEC.md:236 (csrc/wmc_reduce.cu)."""
+    torch = _torch()
+    src, _ = _device_image(img)
+    x, _ = _as_planes(src.contiguous())
+    P, H, W = x.shape
+    nbytes = int(lib().cf_wmc_reduce_workspace_bytes(W, H, P))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    with torch.cuda.device(x.device):
+        check(lib().cf_wmc_energy_f64(x.data_ptr(), W, H, W, P, H * W, float(q), out.data_ptr(),
+                                      ws.data_ptr(), nbytes, _stream_ptr(torch, x.device)),
+              "wmc_energy")
+    return float(out.item())
+
+
+def wmc_histogram(img, scale: float = 255.0, lo: float = -256.0, width: float = 1.0,
+                  nbins: int = 512) -> np.ndarray:
+    """Histogram of wmc_half_laplace values: bins of `width`
+    from `lo` on the `scale`d values (default: the reference's 0-255 scale,
+    width 1 over [-256, 256]); returns int64 counts."""
+    torch = _torch()
+    src, _ = _device_image(img)
+    x, _ = _as_planes(src.contiguous())
+    P, H, W = x.shape
+    nbytes = int(lib().cf_wmc_reduce_workspace_bytes(W, H, P))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    counts = torch.empty(nbins, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        check(lib().cf_wmc_histogram(x.data_ptr(), W, H, W, P, H * W, float(scale), float(lo),
+                                     float(width), int(nbins), counts.data_ptr(), ws.data_ptr(),
+                                     nbytes, _stream_ptr(torch, x.device)), "wmc_histogram")
+    return counts.cpu().numpy()
 
 
 def max_sweeps_per_launch() -> int:

@@ -195,3 +195,22 @@ def test_solve_l2_area_bitexact(lam, dt, iters):
     assert_bitexact(rep.image.cpu().numpy(), ref, f"l2 lam={lam} iters={iters}")
     if lam == 0.0:
         assert_bitexact(rep.image.cpu().numpy(), f, "lambda=0 fixed point")
+
+
+@pytest.mark.parametrize("q", [1.0, 2.0, 0.5])
+def test_wmc_energy_bitexact(q):
+    img = np.stack([cf.synth_image(67, 201, seed=70 + s, n_rects=5, n_discs=5, sigma=0.1)
+                    for s in range(3)])
+    got = cf.wmc_energy(torch.from_numpy(img).cuda(), q)
+    assert got == oracle.wmc_energy(img, q)
+
+
+def test_wmc_energy_general_q_and_histogram():
+    img = cf.synth_image(90, 130, seed=77, n_rects=5, n_discs=5, sigma=0.1)
+    d = torch.from_numpy(img).cuda()
+    got = cf.wmc_energy(d, 1.3)
+    ref = oracle.wmc_energy(img, 1.3)
+    assert abs(got - ref) <= 1e-12 * ref
+    assert np.array_equal(cf.wmc_histogram(d), oracle.wmc_histogram(img))
+    assert np.array_equal(cf.wmc_histogram(d, scale=1000.0, lo=-50.0, width=0.5, nbins=200),
+                          oracle.wmc_histogram(img, 1000.0, -50.0, 0.5, 200))

@@ -328,3 +328,27 @@ def test_l2_area_smooths_toward_data():
     # fixed point of U = f + lam*H^w(U): smoother than f (noise variance down)
     lap = lambda a: a[1:-1, 1:-1] - 0.25 * (a[:-2, 1:-1] + a[2:, 1:-1] + a[1:-1, :-2] + a[1:-1, 2:])  # noqa: E731
     assert lap(u).var() < 0.5 * lap(f).var()
+
+
+# ------------------------------------------------- energies / histogram ----
+def test_wmc_energy_kats():
+    """constant -> 0; WMC energy (q=1) is degree-1
+    homogeneous; the fixed-order sum equals a plain fp64 sum to 1e-12 rel."""
+    assert oracle.wmc_energy(np.full((9, 70), 0.4, np.float32)) == 0.0
+    img = cf.synth_image(50, 77, seed=8, n_rects=5, n_discs=5, sigma=0.1)
+    e1 = oracle.wmc_energy(img, 1.0)
+    assert e1 > 0
+    assert oracle.wmc_energy(2 * img, 1.0) == 2 * e1  # power-of-two scaling is exact
+    plain = float(np.abs(oracle.wmc_map_f32(img).astype(np.float64)).sum())
+    assert abs(e1 - plain) <= 1e-12 * plain
+    e2 = oracle.wmc_energy(img, 2.0)
+    assert abs(e2 - float((oracle.wmc_map_f32(img).astype(np.float64) ** 2).sum())) <= 1e-12 * e2
+
+
+def test_wmc_histogram_kats():
+    """constant corpus -> a single spike at bin 0 (value 0)."""
+    c = oracle.wmc_histogram(np.full((20, 30), 0.7, np.float32))
+    assert c.sum() == 600 and c[256] == 600   # bin of value 0 on [-256, 256)
+    img = cf.synth_image(64, 64, seed=9, n_rects=5, n_discs=5, sigma=0.1)
+    h = oracle.wmc_histogram(img)
+    assert h.sum() == 64 * 64
