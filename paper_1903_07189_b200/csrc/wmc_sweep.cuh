@@ -308,7 +308,8 @@ struct SweepWarp {
     float* dstp;                  // plane base
     const float* fp;              // plane base of f (kModeL2)
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
-    f2 acc[K + 1];
+    uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
+    f2 acc[K + 1][C];             // non-finite accumulators per level and column
     f2 hc[K + 1][C], tm[K + 1][C];  // carried row sums per level and pixel pair
     f2 onv[K + 1][C];               // results of the current step, per level
 
@@ -398,9 +399,9 @@ struct SweepWarp {
             ap = rb + R4[(-2 * L + 2 + 64) & 3];
         }
         f2 m[C + 2], o[C + 2], p[C + 2];
-        lds_nb(am + 8 * C * lane, m);
-        lds_nb(ao + 8 * C * lane, o);
-        lds_nb(ap + 8 * C * lane, p);
+        lds_nb(am + (lbase - sbase), m);
+        lds_nb(ao + (lbase - sbase), o);
+        lds_nb(ap + (lbase - sbase), p);
         if (CHECKED && y == rlo(L)) {  // first row of this level: no carries yet
 #pragma unroll
             for (int j = 1; j <= C; ++j) {
@@ -450,10 +451,10 @@ struct SweepWarp {
                 const f2 r = fma2(o[j], splat(-1.0f), fv);         // f - u
                 const f2 sdir = fma2(splat(P.lambda), hw, r);      // (f-u) + lambda*H
                 nv[j - 1] = fma2(splat(P.dt), sdir, o[j]);
-                if (outc[j - 1]) acc[L] = fma2(nv[j - 1], kZero2, acc[L]);
+                acc[L][j - 1] = fma2(nv[j - 1], kZero2, acc[L][j - 1]);
             } else {
                 nv[j - 1] = fma2(splat(P.dt), hw, o[j]);   // u + dt * H^w
-                if (outc[j - 1]) acc[L] = fma2(nv[j - 1], kZero2, acc[L]);
+                acc[L][j - 1] = fma2(nv[j - 1], kZero2, acc[L][j - 1]);
             }
         }
 #pragma unroll
@@ -531,7 +532,9 @@ struct SweepWarp {
             t_e = min(t_e, min(rhi(L) - 1, P.h - 2) + lag(L));  // y+1 <= h-1, y < rhi
         }
 #pragma unroll
-        for (int L = 0; L <= K; ++L) acc[L] = kZero2;
+        for (int L = 0; L <= K; ++L)
+#pragma unroll
+            for (int j = 0; j < C; ++j) acc[L][j] = kZero2;
         // prologue: rows t_begin .. t_begin+RD-1 (one commit group per row)
 #pragma unroll
         for (int i = 0; i < kRD; ++i) {
@@ -630,6 +633,7 @@ __global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const Swe
     sw.fp = MODE == kModeL2 ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K>();
+    sw.lbase = sw.sbase + 8 * C * sw.lane;
 
     sw.run();
 
@@ -638,9 +642,12 @@ __global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const Swe
             int bad = 0x7fffffff;
 #pragma unroll
             for (int L = K; L >= 1; --L) {
-                const float ax = cfk::lo(sw.acc[L]), ay = cfk::hi(sw.acc[L]);
-                if ((sw.outc[0] || sw.outc[C - 1]) && (ax != ax || (sw.out_h[1] && ay != ay)))
-                    bad = p.iter_base + L;
+#pragma unroll
+                for (int j = 0; j < C; ++j) {  // only this warp's output columns count
+                    const float ax = cfk::lo(sw.acc[L][j]), ay = cfk::hi(sw.acc[L][j]);
+                    if (sw.outc[j] && (ax != ax || (sw.out_h[1] && ay != ay)))
+                        bad = p.iter_base + L;
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(kFull, bad, o));

@@ -214,3 +214,26 @@ def test_wmc_energy_general_q_and_histogram():
     assert np.array_equal(cf.wmc_histogram(d), oracle.wmc_histogram(img))
     assert np.array_equal(cf.wmc_histogram(d, scale=1000.0, lo=-50.0, width=0.5, nbins=200),
                           oracle.wmc_histogram(img, 1000.0, -50.0, 0.5, 200))
+
+
+def test_repeatability_no_races():
+    """The shared-memory rings are warp-private and ordered by __syncwarp;
+    any race would show up as run-to-run differences (compute-sanitizer is
+    not available on this pool)."""
+    img = cf.synth_image(300, 700, seed=99, n_rects=10, n_discs=10, sigma=0.1)
+    d = torch.from_numpy(img).cuda()
+    ref = cf.mc_flow(d, cf.FlowConfig(iters=11)).cpu().numpy()
+    for _ in range(15):
+        assert_bitexact(cf.mc_flow(d, cf.FlowConfig(iters=11)).cpu().numpy(), ref, "repeat")
+    ref_o, _ = oracle.flow_f32(img, 11, 1.0)
+    assert_bitexact(ref, ref_o, "vs oracle")
+
+
+@pytest.mark.parametrize("h,w", [(1, 300007), (300007, 1), (2, 65537), (65537, 3)])
+def test_extreme_aspect_ratios(h, w):
+    img = cf.synth_image(h, w, seed=h + w, n_rects=5, n_discs=5, sigma=0.1)
+    d = torch.from_numpy(img).cuda()
+    assert_bitexact(cf.wmc_half_laplace(d).cpu().numpy(), oracle.wmc_map_f32(img), "map")
+    got = cf.mc_flow(d, cf.FlowConfig(iters=5)).cpu().numpy()
+    ref, _ = oracle.flow_f32(img, 5, 1.0)
+    assert_bitexact(got, ref, f"flow {h}x{w}")
