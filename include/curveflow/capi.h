@@ -103,7 +103,8 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
 
 /* ---------------------------------------------------------------------- */
 /* solve_l2_area, A = identity (Eq. 30 with      */
-/* -dR_area/dU ~ H^w): u <- f, then iters explicit steps                   */
+/* -dR_area/dU ~ H^w): u <- f when init != 0 (else continue from u), then   */
+/* iters explicit steps                                                    */
 /*   U' = U + dt * ((f - U) + lambda * wmc(U))                             */
 /* with wmc the flow's canonical fp32 H^w.  f and u are    */
 /* distinct device images of the same geometry; dt > 0, lambda >= 0.        */
@@ -111,8 +112,27 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
 /* ---------------------------------------------------------------------- */
 CF_API int cf_wmc_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t h,
                                     int64_t pitch, int32_t planes, int64_t plane_stride,
-                                    int32_t iters, float dt, float lambda, void* workspace,
-                                    size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
+                                    int32_t iters, float dt, float lambda, int32_t init,
+                                    void* workspace, size_t workspace_bytes,
+                                    int32_t* first_bad_iter, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* solve_l1_area, A = identity (Eqs. 32-38):      */
+/* init != 0: u <- f, d <- 0; else continue from (u, d).*/
+/* Each of the iters steps, per pixel (fp32):               */
+/*   r = (U - f) + d;  d' = clamp(r, -alpha, alpha)                         */
+/*   U' = U + dt * (lambda * wmc(U) - (2 d' - d) / alpha)                   */
+/* (the shrinkage b = r - d' of Eq. 36 is eliminated).  f, u,  */
+/* d: distinct device images of one geometry; dt > 0, lambda >= 0,          */
+/* 0 < alpha <= 1e30.  Workspace: cf_wmc_solve_l1_area_workspace_bytes.     */
+/* ---------------------------------------------------------------------- */
+CF_API size_t cf_wmc_solve_l1_area_workspace_bytes(int32_t w, int32_t h, int64_t pitch,
+                                                   int32_t planes, int64_t plane_stride);
+CF_API int cf_wmc_solve_l1_area_f32(const float* f, float* u, float* d, int32_t w, int32_t h,
+                                    int64_t pitch, int32_t planes, int64_t plane_stride,
+                                    int32_t iters, float dt, float lambda, float alpha,
+                                    int32_t init, void* workspace, size_t workspace_bytes,
+                                    int32_t* first_bad_iter, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* Row-band primitive for sharded filtering (BASELINE cfg 4).               */
@@ -172,6 +192,14 @@ CF_API int cf_wmc_histogram(const float* img, int32_t w, int32_t h, int64_t pitc
                             int32_t planes, int64_t plane_stride, float scale, float lo,
                             float width, int32_t nbins, uint64_t* d_counts, void* workspace,
                             size_t workspace_bytes, void* stream);
+/* fidelity: *d_out = sum |u - f|^q (f nullable: sum |u|^q), the difference */
+/*   taken in fp64, same fixed order and q handling as the energy; the      */
+/*   solvers' SolveReport series: l1 fidelity q = 1, l2   */
+/*   0.5 * (q = 2), relative update from q = 2 sums.                        */
+CF_API int cf_wmc_fidelity_f64(const float* u, const float* f, int32_t w, int32_t h,
+                               int64_t pitch, int32_t planes, int64_t plane_stride, double q,
+                               double* d_out, void* workspace, size_t workspace_bytes,
+                               void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* Seeded synthetic image generator (BASELINE.json configs). */

@@ -42,6 +42,24 @@ struct FlowConfig {
     enum class Scheme { half_laplace, fd } scheme = Scheme::half_laplace;
 };
 
+// SPEC.md:286-289 with operator A = identity.
+struct SolverConfig {
+    double lambda = 0.0;
+    double alpha = 1.0;   // l1 dual constant
+    double dt = 0.15;
+    int iters = 500;
+    enum class Model { l2_area, l1_area } model = Model::l2_area;
+};
+
+// SPEC.md:290-293 (final state; the per-iteration series are built by the
+// Python SolverConfig.report mode).  fidelity: l2 0.5*||U-f||^2, l1 ||U-f||_1.
+struct SolveReport {
+    Image2D image;
+    Image2D dual;         // l1: final d; empty for l2
+    int iters = 0;
+    double fidelity = 0.0;
+};
+
 class Error : public std::runtime_error {
    public:
     Error(int status, const std::string& what)
@@ -131,6 +149,58 @@ inline Image2D mc_flow(const Image2D& img, const FlowConfig& cfg, cudaStream_t s
                        "D2H");
     detail::cuda_check(cudaStreamSynchronize(s), "sync");
     return out;
+}
+
+// solve_l2_area / solve_l1_area, host in / host out;
+// throws FlowError on divergence.
+inline SolveReport solve(const Image2D& f, const SolverConfig& cfg, cudaStream_t s = nullptr) {
+    const int w = f.width, h = f.height;
+    const int64_t plane = (int64_t)w * h;
+    const size_t n = f.data.size() * sizeof(float);
+    const bool l1 = cfg.model == SolverConfig::Model::l1_area;
+    const size_t wsb = l1 ? cf_wmc_solve_l1_area_workspace_bytes(w, h, w, 1, plane)
+                          : cf_wmc_filter_workspace_bytes(w, h, w, 1, plane);
+    detail::DevBuf df(n), du(n), dd(n), ws(wsb), red(cf_wmc_reduce_workspace_bytes(w, h, 1)),
+        fid(sizeof(double));
+    detail::cuda_check(cudaMemcpyAsync(df.p, f.data.data(), n, cudaMemcpyHostToDevice, s), "H2D");
+    int32_t bad = 0;
+    const int st =
+        l1 ? cf_wmc_solve_l1_area_f32((const float*)df.p, (float*)du.p, (float*)dd.p, w, h, w, 1,
+                                      plane, cfg.iters, (float)cfg.dt, (float)cfg.lambda,
+                                      (float)cfg.alpha, 1, ws.p, wsb, &bad, s)
+           : cf_wmc_solve_l2_area_f32((const float*)df.p, (float*)du.p, w, h, w, 1, plane,
+                                      cfg.iters, (float)cfg.dt, (float)cfg.lambda, 1, ws.p, wsb,
+                                      &bad, s);
+    if (st == CF_ENONFINITE) throw FlowError(bad);
+    detail::check(st, l1 ? "solve_l1_area" : "solve_l2_area");
+    detail::check(cf_wmc_fidelity_f64((const float*)du.p, (const float*)df.p, w, h, w, 1, plane,
+                                      l1 ? 1.0 : 2.0, (double*)fid.p, red.p,
+                                      cf_wmc_reduce_workspace_bytes(w, h, 1), s),
+                  "fidelity");
+    SolveReport rep;
+    rep.image = Image2D(w, h);
+    rep.iters = cfg.iters;
+    detail::cuda_check(cudaMemcpyAsync(rep.image.data.data(), du.p, n, cudaMemcpyDeviceToHost, s),
+                       "D2H");
+    if (l1) {
+        rep.dual = Image2D(w, h);
+        detail::cuda_check(
+            cudaMemcpyAsync(rep.dual.data.data(), dd.p, n, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    double fv = 0.0;
+    detail::cuda_check(cudaMemcpyAsync(&fv, fid.p, sizeof(double), cudaMemcpyDeviceToHost, s),
+                       "D2H");
+    detail::cuda_check(cudaStreamSynchronize(s), "sync");
+    rep.fidelity = l1 ? fv : 0.5 * fv;
+    return rep;
+}
+inline SolveReport solve_l2_area(const Image2D& f, SolverConfig cfg, cudaStream_t s = nullptr) {
+    cfg.model = SolverConfig::Model::l2_area;
+    return solve(f, cfg, s);
+}
+inline SolveReport solve_l1_area(const Image2D& f, SolverConfig cfg, cudaStream_t s = nullptr) {
+    cfg.model = SolverConfig::Model::l1_area;
+    return solve(f, cfg, s);
 }
 
 // Per-channel processing: planes are independent.

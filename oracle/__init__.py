@@ -41,8 +41,15 @@ def lib():
         L.or_quantize_u8.argtypes = [_vp, _vp, _i64]
         L.or_quantize_u8.restype = None
         L.or_solve_l2_area_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32,
-                                           _f32, _i32, _pi32]
+                                           _f32, _i32, _i32, _pi32]
         L.or_solve_l2_area_f32.restype = C.c_int
+        L.or_solve_l1_area_f32.argtypes = [_vp, _vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32,
+                                           _f32, _f32, _f32, _i32, _i32, _pi32]
+        L.or_solve_l1_area_f32.restype = C.c_int
+        L.or_l1_px.argtypes = [_f32, _f32, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+        L.or_l1_px.restype = None
+        L.or_fidelity.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _f64, _i32]
+        L.or_fidelity.restype = C.c_double
         L.or_energy_from_map.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32]
         L.or_energy_from_map.restype = C.c_double
         L.or_histogram_from_map.argtypes = [_vp, _i64, _f32, _f32, _f32, _i32, _vp]
@@ -195,17 +202,61 @@ def flow_image8(img8, iters, dt=1.0, threads=None):
     return (q[0] if a.ndim == 2 else np.ascontiguousarray(np.moveaxis(q, 0, 2))), bad
 
 
-def solve_l2_area_f32(f, iters, dt, lam, threads=None):
-    """fp32 canonical solve_l2_area (A = I); returns (U^iters, bad_iter)."""
+def solve_l2_area_f32(f, iters, dt, lam, threads=None, u0=None):
+    """fp32 canonical solve_l2_area (A = I); returns (U^iters, bad_iter).
+    u0: continue from this iterate instead of U^0 = f."""
     a = np.ascontiguousarray(f, dtype=np.float32)
     a3 = a[None] if a.ndim == 2 else a
     P, h, w = a3.shape
-    u = np.empty_like(a3)
+    u = (np.empty_like(a3) if u0 is None
+         else np.array(np.asarray(u0, np.float32).reshape(a3.shape), copy=True))
     bad = C.c_int32(0)
     rc = lib().or_solve_l2_area_f32(a3.ctypes.data, u.ctypes.data, w, h, w, P, h * w, int(iters),
-                                    float(dt), float(lam), _threads(threads), C.byref(bad))
+                                    float(dt), float(lam), int(u0 is None), _threads(threads),
+                                    C.byref(bad))
     assert rc in (0, 3), rc
     return (u[0] if a.ndim == 2 else u), bad.value
+
+
+def solve_l1_area_f32(f, iters, dt, lam, alpha, threads=None, state=None):
+    """fp32 canonical solve_l1_area (A = I); returns (U, d, bad_iter).
+    state = (u0, d0): continue from that iterate instead of U^0 = f, d^0 = 0."""
+    a = np.ascontiguousarray(f, dtype=np.float32)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    if state is None:
+        u, d = np.empty_like(a3), np.empty_like(a3)
+    else:
+        u = np.array(np.asarray(state[0], np.float32).reshape(a3.shape), copy=True)
+        d = np.array(np.asarray(state[1], np.float32).reshape(a3.shape), copy=True)
+    bad = C.c_int32(0)
+    rc = lib().or_solve_l1_area_f32(a3.ctypes.data, u.ctypes.data, d.ctypes.data, w, h, w, P,
+                                    h * w, int(iters), float(dt), float(lam), float(alpha),
+                                    int(state is None), _threads(threads), C.byref(bad))
+    assert rc in (0, 3), rc
+    if a.ndim == 2:
+        return u[0], d[0], bad.value
+    return u, d, bad.value
+
+
+def l1_px(r, alpha):
+    """Eq. 36 shrinkage b and Eq. 37 dual d' for one residual (fp32)."""
+    b, d = C.c_float(0), C.c_float(0)
+    lib().or_l1_px(float(r), float(alpha), C.byref(b), C.byref(d))
+    return b.value, d.value
+
+
+def fidelity(u, f=None, q=1.0):
+    """Fixed-order sum |u - f|^q (f None: sum |u|^q), as cf_wmc_fidelity_f64."""
+    a = np.ascontiguousarray(u, dtype=np.float32)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    b3 = None
+    if f is not None:
+        b3 = np.ascontiguousarray(f, dtype=np.float32).reshape(a3.shape)
+    qk = 1 if q == 1.0 else (2 if q == 2.0 else (3 if q == 0.5 else 0))
+    return lib().or_fidelity(a3.ctypes.data, None if b3 is None else b3.ctypes.data, w, h, w, P,
+                             h * w, float(q), qk)
 
 
 def wmc_energy(img, q=1.0, threads=None):

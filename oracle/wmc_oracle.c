@@ -262,7 +262,8 @@ static void l2_row(void* vctx, int y) {
 
 OR_EXPORT int or_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t h, int64_t pitch,
                                    int32_t planes, int64_t plane_stride, int32_t iters, float dt,
-                                   float lambda, int32_t threads, int32_t* bad_iter) {
+                                   float lambda, int32_t init, int32_t threads,
+                                   int32_t* bad_iter) {
     if (w <= 0 || h <= 0 || planes <= 0 || iters < 0 || pitch < w) return 1;
     if (bad_iter) *bad_iter = 0;
     float* tmp = (float*)malloc(sizeof(float) * (size_t)pitch * (size_t)h);
@@ -271,7 +272,7 @@ OR_EXPORT int or_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t 
     for (int p = 0; p < planes && rc == 0; ++p) {
         float* U = u + p * plane_stride;
         const float* F = f + p * plane_stride;
-        memcpy(U, F, sizeof(float) * (size_t)pitch * (size_t)h);
+        if (init) memcpy(U, F, sizeof(float) * (size_t)pitch * (size_t)h);
         float *A = U, *B = tmp;
         for (int t = 1; t <= iters; ++t) {
             memset(bad, 0, sizeof(int) * (size_t)h);
@@ -285,6 +286,91 @@ OR_EXPORT int or_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t 
         if (A != U) memcpy(U, A, sizeof(float) * (size_t)pitch * (size_t)h);
     }
     free(tmp);
+    free(bad);
+    return rc;
+}
+
+/* solve_l1_area with A = I (Eqs. 32-38), one
+ * iteration per pixel in fp32 (the kernel's kModeL1):
+ *   r  = fl(fl(u - f) + d)                 (fmaf(f, -1, u) then +)
+ *   d' = fminf(fmaxf(r, -alpha), alpha)    (Eq. 37; NaN r -> -alpha)
+ *   e  = fmaf(d, -1, d' + d')              (2d' - d; d' + d' exact)
+ *   s  = fmaf(lambda, H^w(U), e * nia)     (nia = -fl(1/alpha))
+ *   U' = fmaf(dt, s, u)
+ * The shrinkage b = r - d' (Eq. 36) never enters the update;
+ * or_l1_px exposes it for the KATs.  init: U = f, d = 0. */
+OR_EXPORT void or_l1_px(float r, float alpha, float* b, float* d_new) {
+    /* Eq. 36 branches and Eq. 37's clamp, literally */
+    *b = r > alpha ? r - alpha : (r < -alpha ? r + alpha : 0.0f);
+    *d_new = fminf(fmaxf(r, -alpha), alpha);
+}
+
+typedef struct {
+    const float* in;
+    const float* f;
+    const float* d;
+    float* out;
+    float* dout;
+    int w, h;
+    int64_t pitch;
+    float dt, lambda, alpha, nia;
+    volatile int* bad;
+} l1_ctx;
+
+static void l1_row(void* vctx, int y) {
+    l1_ctx* c = (l1_ctx*)vctx;
+    int bad = 0;
+    for (int x = 0; x < c->w; ++x) {
+        const int64_t i = (int64_t)y * c->pitch + x;
+        const float u = c->in[i], dv = c->d[i];
+        const float hw = wmc_at_f32(c->in, c->w, c->h, c->pitch, y, x, 0, NULL);
+        const float r = fmaf(c->f[i], -1.0f, u) + dv;
+        const float dn = fminf(fmaxf(r, -c->alpha), c->alpha);
+        const float e = fmaf(dv, -1.0f, dn + dn);
+        const float v = fmaf(c->dt, fmaf(c->lambda, hw, e * c->nia), u);
+        if (!isfinite(v)) bad = 1;
+        c->out[i] = v;
+        c->dout[i] = dn;
+    }
+    if (bad) c->bad[y] = 1;
+}
+
+OR_EXPORT int or_solve_l1_area_f32(const float* f, float* u, float* d, int32_t w, int32_t h,
+                                   int64_t pitch, int32_t planes, int64_t plane_stride,
+                                   int32_t iters, float dt, float lambda, float alpha,
+                                   int32_t init, int32_t threads, int32_t* bad_iter) {
+    if (w <= 0 || h <= 0 || planes <= 0 || iters < 0 || pitch < w || !(alpha > 0.0f)) return 1;
+    if (bad_iter) *bad_iter = 0;
+    const size_t n = (size_t)pitch * (size_t)h;
+    float* tmp = (float*)malloc(sizeof(float) * n);
+    float* dtmp = (float*)malloc(sizeof(float) * n);
+    int* bad = (int*)calloc((size_t)h, sizeof(int));
+    const float nia = -(1.0f / alpha);
+    int rc = 0;
+    for (int p = 0; p < planes && rc == 0; ++p) {
+        float* U = u + p * plane_stride;
+        float* D = d + p * plane_stride;
+        const float* F = f + p * plane_stride;
+        if (init) {
+            memcpy(U, F, sizeof(float) * n);
+            memset(D, 0, sizeof(float) * n);
+        }
+        float *A = U, *B = tmp, *DA = D, *DB = dtmp;
+        for (int t = 1; t <= iters; ++t) {
+            memset(bad, 0, sizeof(int) * (size_t)h);
+            l1_ctx c = {A, F, DA, B, DB, w, h, pitch, dt, lambda, alpha, nia, bad};
+            for_rows(h, threads, l1_row, &c);
+            float* s = A; A = B; B = s;
+            s = DA; DA = DB; DB = s;
+            int any = 0;
+            for (int y = 0; y < h; ++y) any |= bad[y];
+            if (any) { if (bad_iter) *bad_iter = t; rc = 3; break; }
+        }
+        if (A != U) memcpy(U, A, sizeof(float) * n);
+        if (DA != D) memcpy(D, DA, sizeof(float) * n);
+    }
+    free(tmp);
+    free(dtmp);
     free(bad);
     return rc;
 }
@@ -307,6 +393,37 @@ OR_EXPORT double or_energy_from_map(const float* map, int32_t w, int32_t h, int3
                     const int x = x0 + l;
                     if (x >= w) { v[l] = 0.0; continue; }
                     const double a = fabs((double)r[x]);
+                    v[l] = qkind == 1 ? a : (qkind == 2 ? a * a : (qkind == 3 ? sqrt(a) : pow(a, q)));
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    double nv[32];
+                    for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ o];
+                    memcpy(v, nv, sizeof(v));
+                }
+                row = row + v[0];
+            }
+            total = total + row;
+        }
+    return total;
+}
+
+/* Fidelity sum |u - f|^q (f NULL: sum |u|^q) over pitched planes, the
+ * difference in fp64, in the energy's fixed order (wmc_reduce.cu
+ * row_fidelity_kernel). */
+OR_EXPORT double or_fidelity(const float* u, const float* f, int32_t w, int32_t h, int64_t pitch,
+                             int32_t planes, int64_t plane_stride, double q, int32_t qkind) {
+    double total = 0.0;
+    for (int p = 0; p < planes; ++p)
+        for (int y = 0; y < h; ++y) {
+            const int64_t off = (int64_t)p * plane_stride + (int64_t)y * pitch;
+            double row = 0.0;
+            for (int x0 = 0; x0 < w; x0 += 32) {
+                double v[32];
+                for (int l = 0; l < 32; ++l) {
+                    const int x = x0 + l;
+                    if (x >= w) { v[l] = 0.0; continue; }
+                    const double a =
+                        fabs(f ? (double)u[off + x] - (double)f[off + x] : (double)u[off + x]);
                     v[l] = qkind == 1 ? a : (qkind == 2 ? a * a : (qkind == 3 ? sqrt(a) : pow(a, q)));
                 }
                 for (int o = 16; o > 0; o >>= 1) {

@@ -40,7 +40,10 @@ SIGNATURES = {
     "cf_wmc_filter_u8_f32": (C.c_int, [_vp, _i64, _i64, _vp, _i32, _i32, _i64, _i32, _i64,
                                        _i32, _f32, _vp, _sz, _pi32, _vp]),
     "cf_wmc_solve_l2_area_f32": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32,
-                                           _f32, _vp, _sz, _pi32, _vp]),
+                                           _f32, _i32, _vp, _sz, _pi32, _vp]),
+    "cf_wmc_solve_l1_area_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32, _i64]),
+    "cf_wmc_solve_l1_area_f32": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32,
+                                           _f32, _f32, _f32, _i32, _vp, _sz, _pi32, _vp]),
     "cf_wmc_max_sweeps_per_launch": (_i32, []),
     "cf_wmc_filter_launches": (_i32, [_i32]),
     "cf_wmc_sweeps_band_f32": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i32,
@@ -54,6 +57,8 @@ SIGNATURES = {
     "cf_wmc_energy_f64": (C.c_int, [_vp, _i32, _i32, _i64, _i32, _i64, _f64, _vp, _vp, _sz, _vp]),
     "cf_wmc_histogram": (C.c_int, [_vp, _i32, _i32, _i64, _i32, _i64, _f32, _f32, _f32, _i32,
                                    _vp, _vp, _sz, _vp]),
+    "cf_wmc_fidelity_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _f64, _vp, _vp,
+                                      _sz, _vp]),
     "cf_synth_f32": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_synth_u8": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_kernel_bank_x12": (None, [_pi32]),

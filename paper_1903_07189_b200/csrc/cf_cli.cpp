@@ -8,6 +8,8 @@
 //   curveflow_b200 op    --size H W --seed S           -> checksum of the map
 //   curveflow_b200 flow  --size H W --iters N --dt D   -> checksum of U^N
 //   curveflow_b200 bench --size H W --iters N --reps R -> Gpixel-updates/s
+//   curveflow_b200 smooth --model l1|l2 --lambda L --alpha A --iters N --dt D
+//                                                       -> checksum of U
 //
 // Output: one JSON object per invocation on stdout.
 #include <cuda_runtime.h>
@@ -35,14 +37,17 @@ uint64_t fnv1a(const std::vector<float>& v) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::fprintf(stderr, "usage: %s op|flow|bench [--size H W] [--seed S] [--iters N] "
-                             "[--dt D] [--reps R]\n", argv[0]);
+        std::fprintf(stderr, "usage: %s op|flow|bench|smooth [--size H W] [--seed S] "
+                             "[--iters N] [--dt D] [--reps R] [--model l1|l2] [--lambda L] "
+                             "[--alpha A]\n", argv[0]);
         return 2;
     }
     const std::string cmd = argv[1];
     int H = 512, W = 512, iters = 100, reps = 3;
     uint64_t seed = 1;
-    double dt = 1.0;
+    double dt = 1.0, lambda = 0.0, alpha = 1.0;
+    bool dt_set = false;
+    std::string model = "l2";
     for (int i = 2; i < argc; ++i) {
         if (!std::strcmp(argv[i], "--size") && i + 2 < argc) {
             H = std::atoi(argv[++i]);
@@ -53,6 +58,13 @@ int main(int argc, char** argv) {
             iters = std::atoi(argv[++i]);
         } else if (!std::strcmp(argv[i], "--dt") && i + 1 < argc) {
             dt = std::atof(argv[++i]);
+            dt_set = true;
+        } else if (!std::strcmp(argv[i], "--model") && i + 1 < argc) {
+            model = argv[++i];
+        } else if (!std::strcmp(argv[i], "--lambda") && i + 1 < argc) {
+            lambda = std::atof(argv[++i]);
+        } else if (!std::strcmp(argv[i], "--alpha") && i + 1 < argc) {
+            alpha = std::atof(argv[++i]);
         } else if (!std::strcmp(argv[i], "--reps") && i + 1 < argc) {
             reps = std::atoi(argv[++i]);
         }
@@ -68,6 +80,19 @@ int main(int argc, char** argv) {
             auto u = curveflow::cuda::mc_flow(img, {dt, iters});
             std::printf("{\"op\": \"flow\", \"h\": %d, \"w\": %d, \"iters\": %d, \"fnv1a\": "
                         "\"%016llx\"}\n", H, W, iters, (unsigned long long)fnv1a(u.data));
+        } else if (cmd == "smooth") {
+            curveflow::SolverConfig cfg;
+            cfg.lambda = lambda;
+            cfg.alpha = alpha;
+            cfg.iters = iters;
+            if (dt_set) cfg.dt = dt;  // else the SPEC default 0.15
+            if (model == "l1") cfg.model = curveflow::SolverConfig::Model::l1_area;
+            else if (model != "l2") throw std::invalid_argument("--model must be l1 or l2");
+            auto rep = curveflow::cuda::solve(img, cfg);
+            std::printf("{\"op\": \"smooth\", \"model\": \"%s\", \"h\": %d, \"w\": %d, "
+                        "\"iters\": %d, \"fidelity\": %.17g, \"fnv1a\": \"%016llx\"}\n",
+                        model.c_str(), H, W, iters, rep.fidelity,
+                        (unsigned long long)fnv1a(rep.image.data));
         } else if (cmd == "bench") {
             // device-resident timing of mc_flow (SPEC.md:437-456 median of reps)
             const size_t n = img.data.size() * sizeof(float);

@@ -244,9 +244,13 @@ CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch,
     return kWsHeader + (size_t)elems * sizeof(float);
 }
 
-struct DataTerm {            // solve_l2_area: U' = U + dt*((f - U) + lambda*H^w)
+struct DataTerm {            // solve_l2_area / solve_l1_area (f != nullptr)
     const float* f = nullptr;
     float lambda = 0.0f;
+    // solve_l1_area only (d != nullptr): dual planes, ping-ponged with d_ws
+    float* d = nullptr;
+    float* d_ws = nullptr;
+    float alpha = 1.0f;
 };
 
 static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t src_plane,
@@ -264,6 +268,8 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
     // the last launch writes `out` (even launch count; iters == 1 copies).
     float* cur = out;
     float* nxt = ws;
+    float* dcur = dterm.d;      // kModeL1: follows the same ping-pong as U
+    float* dnxt = dterm.d_ws;
     if (src_u8) {
         // widen u8 -> fp32 into whichever buffer makes the
         // final launch land in `out`
@@ -283,17 +289,26 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
         p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
         p.dt = dt; p.iter_base = iter; p.flag = flag;
         p.fdata = dterm.f; p.f_pitch = pitch; p.f_plane = plane_stride; p.lambda = dterm.lambda;
-        const int rc = dterm.f ? launch<cfk::kModeL2>(p, ks[i], d, s)
-                               : launch<cfk::kModeFlow>(p, ks[i], d, s);
+        p.dsrc = dcur; p.ddst = dnxt;
+        p.alpha = dterm.alpha; p.neg_inv_alpha = -(1.0f / dterm.alpha);
+        const int rc = dterm.d   ? launch<cfk::kModeL1>(p, ks[i], d, s)
+                       : dterm.f ? launch<cfk::kModeL2>(p, ks[i], d, s)
+                                 : launch<cfk::kModeFlow>(p, ks[i], d, s);
         if (rc) return rc;
         iter += ks[i];
         std::swap(cur, nxt);
+        std::swap(dcur, dnxt);
     }
     if (cur != out) {
         // iters == 1 on an in-place f32 image: the single launch wrote ws
         for (int pl = 0; pl < planes; ++pl)
             CF_CUDA(cudaMemcpy2DAsync(out + pl * plane_stride, pitch * 4, cur + pl * plane_stride,
                                       pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
+        if (dterm.d)
+            for (int pl = 0; pl < planes; ++pl)
+                CF_CUDA(cudaMemcpy2DAsync(dterm.d + pl * plane_stride, pitch * 4,
+                                          dcur + pl * plane_stride, pitch * 4, (size_t)w * 4, h,
+                                          cudaMemcpyDeviceToDevice, s));
     }
     if (first_bad_iter) return cf_wmc_filter_query_nonfinite(workspace, first_bad_iter, s);
     return CF_OK;
@@ -339,17 +354,19 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
 
 CF_API int cf_wmc_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t h,
                                     int64_t pitch, int32_t planes, int64_t plane_stride,
-                                    int32_t iters, float dt, float lambda, void* workspace,
-                                    size_t workspace_bytes, int32_t* first_bad_iter, void* stream) {
+                                    int32_t iters, float dt, float lambda, int32_t init,
+                                    void* workspace, size_t workspace_bytes,
+                                    int32_t* first_bad_iter, void* stream) {
     if (!f || !u || f == u || !shape_ok(w, h, pitch, planes, plane_stride) || iters < 0)
         return CF_EINVAL;
     if (!(dt > 0.0f) || !(dt < 3.0e38f) || !(lambda >= 0.0f) || !(lambda < 3.0e38f))
         return CF_EINVAL;
     if (first_bad_iter) *first_bad_iter = 0;
     cudaStream_t s = (cudaStream_t)stream;
-    for (int pl = 0; pl < planes; ++pl)  // U^0 = f
-        CF_CUDA(cudaMemcpy2DAsync(u + pl * plane_stride, pitch * 4, f + pl * plane_stride,
-                                  pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
+    if (init)
+        for (int pl = 0; pl < planes; ++pl)  // U^0 = f
+            CF_CUDA(cudaMemcpy2DAsync(u + pl * plane_stride, pitch * 4, f + pl * plane_stride,
+                                      pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
     if (iters == 0) return CF_OK;
     if (!workspace ||
         workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))
@@ -357,6 +374,51 @@ CF_API int cf_wmc_solve_l2_area_f32(const float* f, float* u, int32_t w, int32_t
     DataTerm dterm;
     dterm.f = f;
     dterm.lambda = lambda;
+    return run_flow(u, false, pitch, plane_stride, u, w, h, pitch, planes, plane_stride, iters,
+                    dt, workspace, first_bad_iter, s, dterm);
+}
+
+CF_API size_t cf_wmc_solve_l1_area_workspace_bytes(int32_t w, int32_t h, int64_t pitch,
+                                                   int32_t planes, int64_t plane_stride) {
+    if (!shape_ok(w, h, pitch, planes, plane_stride)) return 0;
+    const int64_t elems = (planes - 1) * (planes > 1 ? plane_stride : 0) + pitch * (int64_t)h;
+    const size_t img = ((size_t)elems * sizeof(float) + 255) & ~(size_t)255;
+    return kWsHeader + img + (size_t)elems * sizeof(float);
+}
+
+CF_API int cf_wmc_solve_l1_area_f32(const float* f, float* u, float* d, int32_t w, int32_t h,
+                                    int64_t pitch, int32_t planes, int64_t plane_stride,
+                                    int32_t iters, float dt, float lambda, float alpha,
+                                    int32_t init, void* workspace, size_t workspace_bytes,
+                                    int32_t* first_bad_iter, void* stream) {
+    if (!f || !u || !d || f == u || f == d || u == d ||
+        !shape_ok(w, h, pitch, planes, plane_stride) || iters < 0)
+        return CF_EINVAL;
+    if (!(dt > 0.0f) || !(dt < 3.0e38f) || !(lambda >= 0.0f) || !(lambda < 3.0e38f))
+        return CF_EINVAL;
+    if (!(alpha > 0.0f) || !(alpha <= 1.0e30f)) return CF_EINVAL;
+    if (first_bad_iter) *first_bad_iter = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (init) {
+        for (int pl = 0; pl < planes; ++pl) {  // U^0 = f, d^0 = 0
+            CF_CUDA(cudaMemcpy2DAsync(u + pl * plane_stride, pitch * 4, f + pl * plane_stride,
+                                      pitch * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
+            CF_CUDA(cudaMemset2DAsync(d + pl * plane_stride, pitch * 4, 0, (size_t)w * 4, h, s));
+        }
+    }
+    if (iters == 0) return CF_OK;
+    if (!workspace ||
+        workspace_bytes < cf_wmc_solve_l1_area_workspace_bytes(w, h, pitch, planes, plane_stride))
+        return CF_EINVAL;
+    const int64_t elems = (planes - 1) * (planes > 1 ? plane_stride : 0) + pitch * (int64_t)h;
+    DataTerm dterm;
+    dterm.f = f;
+    dterm.lambda = lambda;
+    dterm.d = d;
+    dterm.d_ws = reinterpret_cast<float*>(
+        reinterpret_cast<char*>(workspace) + kWsHeader +
+        (((size_t)elems * sizeof(float) + 255) & ~(size_t)255));
+    dterm.alpha = alpha;
     return run_flow(u, false, pitch, plane_stride, u, w, h, pitch, planes, plane_stride, iters,
                     dt, workspace, first_bad_iter, s, dterm);
 }

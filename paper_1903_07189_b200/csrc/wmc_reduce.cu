@@ -1,6 +1,6 @@
 // paper_1903_07189_b200/csrc/wmc_reduce.cu -- reductions over the WMC map
 // (SURVEY.md §8f rank 2): the WMC regularisation energy and the WMC value
-// histogram.
+// histogram; plus the solvers' data-fidelity sums (SolveReport series).
 //
 // Reference semantics:
 //  * energy(img, kind = WMC, q) = sum over pixels of |H^w|^q with H^w from
@@ -31,14 +31,43 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ double term(float hw, double q, int qkind) {
-    const double a = fabs((double)hw);
+__device__ __forceinline__ double term_abs(double a, double q, int qkind) {
     switch (qkind) {
         case 1: return a;
         case 2: return __dmul_rn(a, a);
         case 3: return __dsqrt_rn(a);
         default: return pow(a, q);
     }
+}
+
+__device__ __forceinline__ double term(float hw, double q, int qkind) {
+    return term_abs(fabs((double)hw), q, qkind);
+}
+
+// One warp per row of |u - f|^q (f nullable), same block order as the energy.
+__global__ void row_fidelity_kernel(const float* __restrict__ u, const float* __restrict__ f,
+                                    int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                                    int64_t plane_stride, double q, int qkind,
+                                    double* __restrict__ row_sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= (int64_t)h * planes) return;
+    const int64_t p = row / h, y = row % h;
+    const int64_t off = p * plane_stride + y * pitch;
+    double acc = 0.0;
+    for (int x0 = 0; x0 < w; x0 += 32) {
+        const int x = x0 + lane;
+        double v = 0.0;
+        if (x < w) {
+            const double a = f ? __dsub_rn((double)u[off + x], (double)f[off + x])
+                               : (double)u[off + x];
+            v = term_abs(fabs(a), q, qkind);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
+        acc = __dadd_rn(acc, v);
+    }
+    if (lane == 0) row_sums[row] = acc;
 }
 
 // One warp per row: block sums by xor butterfly, sequential over blocks.
@@ -129,6 +158,24 @@ CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pit
     const int64_t nrows = (int64_t)h * planes;
     row_energy_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(
         map, w, h, w, planes, (int64_t)w * h, q, qkind_of(q), rows);
+    ordered_sum_kernel<<<1, 32, 0, s>>>(rows, nrows, d_out);
+    return fail();
+}
+
+CF_API int cf_wmc_fidelity_f64(const float* u, const float* f, int32_t w, int32_t h,
+                               int64_t pitch, int32_t planes, int64_t plane_stride, double q,
+                               double* d_out, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+    if (!u || !d_out || !workspace || w <= 0 || h <= 0 || planes <= 0 || pitch < w)
+        return CF_EINVAL;
+    if (planes > 1 && plane_stride < pitch * (int64_t)h) return CF_EINVAL;
+    if (!(q > 0.0) || !(q < 1e300)) return CF_EINVAL;
+    if (workspace_bytes < cf_wmc_reduce_workspace_bytes(w, h, planes)) return CF_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    double* rows = reinterpret_cast<double*>(workspace);
+    const int64_t nrows = (int64_t)h * planes;
+    row_fidelity_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(
+        u, f, w, h, pitch, planes, plane_stride, q, qkind_of(q), rows);
     ordered_sum_kernel<<<1, 32, 0, s>>>(rows, nrows, d_out);
     return fail();
 }

@@ -80,12 +80,18 @@ struct SweepParams {
     const float* fdata;       // global row 0 of plane 0 (same column geometry as src)
     int64_t f_pitch, f_plane; // elements
     float lambda;
+    // MODE == kModeL1 (solve_l1_area): dual planes d (geometry of f)
+    const float* dsrc;        // d^t, global row 0 of plane 0
+    float* ddst;              // d^{t+K} (output columns/rows only)
+    float alpha;              // dual clamp
+    float neg_inv_alpha;      // -fl(1/alpha)
 };
 
 // Per-pixel update a launch applies at every level.
 constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_flow)
 constexpr int kModeMap = 1;   // out = H^w(U), one level, fp64 near-tie rule (wmc_half_laplace)
 constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)
+constexpr int kModeL1 = 3;    // primal-dual step of solve_l1_area
 
 // Column geometry for K levels: each chunk window overlaps its neighbours by
 // A = K columns per side (the trapezoid shrinks one column per level).
@@ -242,6 +248,9 @@ __device__ __forceinline__ void pair_d(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e,
 }
 
 __device__ __forceinline__ f2 select_pair(const PairD& P) {
+#ifdef CF_EXP_NOSELECT  // diagnostic builds only (wrong results): cost of the selection
+    return P.d[0];
+#endif
     return pk(select8(lo(P.d[0]), lo(P.d[1]), lo(P.d[2]), lo(P.d[3]), lo(P.d[4]), lo(P.d[5]),
                       lo(P.d[6]), lo(P.d[7])),
               select8(hi(P.d[0]), hi(P.d[1]), hi(P.d[2]), hi(P.d[3]), hi(P.d[4]), hi(P.d[5]),
@@ -306,12 +315,18 @@ struct SweepWarp {
     __device__ __forceinline__ int rhi(int L) const { return min(ye + (K - L), P.h); }
     const float* srcp;            // plane base
     float* dstp;                  // plane base
-    const float* fp;              // plane base of f (kModeL2)
+    const float* fp;              // plane base of f (kModeL2, kModeL1)
+    const float* dsp;             // plane base of d^t (kModeL1)
+    float* ddp;                   // plane base of d^{t+K} (kModeL1)
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
     f2 acc[K + 1][C];             // non-finite accumulators per level and column
     f2 hc[K + 1][C], tm[K + 1][C];  // carried row sums per level and pixel pair
     f2 onv[K + 1][C];               // results of the current step, per level
+    // kModeL1: the dual d_L(y) a level produces is consumed pointwise by
+    // level L+1 two steps later (same lane, same columns): a 2-deep register
+    // FIFO per level (odv -> dmid -> dold), shifted once per step.
+    f2 odv[K + 1][C], dmid[K + 1][C], dold[K + 1][C];
 
     __device__ __forceinline__ SweepWarp(const SweepParams& p) : P(p) {}
 
@@ -372,6 +387,19 @@ struct SweepWarp {
                 }
             }
         }
+    }
+
+    // Pointwise pair {plane[y][xf[0]+jj], plane[y][xf[1]+jj]} of an f-geometry
+    // plane (data term / dual); CHECKED clamps the columns of border warps.
+    template <bool CHECKED>
+    __device__ __forceinline__ f2 ld_pt(const float* plane, int y, int jj) const {
+        const float* row = plane + (int64_t)y * P.f_pitch;
+        int x0 = xf[0] + jj, x1 = xf[1] + jj;
+        if (CHECKED) {
+            x0 = min(max(x0, 0), P.w - 1);
+            x1 = min(max(x1, 0), P.w - 1);
+        }
+        return pk(__ldg(row + x0), __ldg(row + x1));
     }
 
     // Compute level L's row for step t.  CHECKED: range check, clamped row
@@ -441,16 +469,26 @@ struct SweepWarp {
                 nv[j - 1] = hw;
             } else if constexpr (MODE == kModeL2) {
                 // SPEC.md:298 with A = I: U' = U + dt*((f - U) + lambda*H^w(U))
-                const float* frow = fp + (int64_t)y * P.f_pitch;
-                int x0 = xf[0] + j - 1, x1 = xf[1] + j - 1;
-                if (CHECKED) {
-                    x0 = min(max(x0, 0), P.w - 1);
-                    x1 = min(max(x1, 0), P.w - 1);
-                }
-                const f2 fv = pk(__ldg(frow + x0), __ldg(frow + x1));
+                const f2 fv = ld_pt<CHECKED>(fp, y, j - 1);
                 const f2 r = fma2(o[j], splat(-1.0f), fv);         // f - u
                 const f2 sdir = fma2(splat(P.lambda), hw, r);      // (f-u) + lambda*H
                 nv[j - 1] = fma2(splat(P.dt), sdir, o[j]);
+                acc[L][j - 1] = fma2(nv[j - 1], kZero2, acc[L][j - 1]);
+            } else if constexpr (MODE == kModeL1) {
+                // SPEC.md:306 with A = I:
+                //   r = (u - f) + d;  d' = clamp(r, -alpha, alpha)
+                //   U' = u + dt*(lambda*H^w - (2d' - d)/alpha)
+                const f2 fv = ld_pt<CHECKED>(fp, y, j - 1);
+                f2 dv;
+                if constexpr (L == 1) dv = ld_pt<CHECKED>(dsp, y, j - 1);
+                else dv = dold[L - 1][j - 1];
+                const f2 r = add2(fma2(fv, splat(-1.0f), o[j]), dv);
+                const f2 dn = pk(fminf(fmaxf(lo(r), -P.alpha), P.alpha),
+                                 fminf(fmaxf(hi(r), -P.alpha), P.alpha));
+                const f2 e = fma2(dv, splat(-1.0f), add2(dn, dn));  // 2d' - d
+                const f2 sdir = fma2(splat(P.lambda), hw, mul2(e, splat(P.neg_inv_alpha)));
+                nv[j - 1] = fma2(splat(P.dt), sdir, o[j]);
+                odv[L][j - 1] = dn;
                 acc[L][j - 1] = fma2(nv[j - 1], kZero2, acc[L][j - 1]);
             } else {
                 nv[j - 1] = fma2(splat(P.dt), hw, o[j]);   // u + dt * H^w
@@ -475,6 +513,15 @@ struct SweepWarp {
         const int y = t - lag(L);
         if (CHECKED && (y < rlo(L) || y >= rhi(L))) return;  // warp-uniform
         const f2 (&nv)[C] = onv[L];
+        if constexpr (L == K && MODE == kModeL1) {
+            float* drow = ddp + (int64_t)y * P.f_pitch;
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                if (!outc[j]) continue;
+                if (out_h[0] && (!CHECKED || xf[0] + j < P.w)) drow[xf[0] + j] = lo(odv[K][j]);
+                if (out_h[1] && (!CHECKED || xf[1] + j < P.w)) drow[xf[1] + j] = hi(odv[K][j]);
+            }
+        }
         if constexpr (L == K) {
             if (CHECKED) {
                 float* row = dstp + (int64_t)(y - P.dst_row0) * P.dst_pitch;
@@ -518,6 +565,20 @@ struct SweepWarp {
         const int y = t - lag(L);
         if (y >= rlo(L) && y < rhi(L)) clamp_row(row_addr<L>(y));
         if constexpr (L + 1 < K) clamp_levels<L + 1>(t);
+    }
+
+    // kModeL1: end of step -- level L's dual of row t-lag(L) becomes level
+    // L+1's input at step t+2 (rows outside a level's range are never read).
+    __device__ __forceinline__ void shift_duals() {
+        if constexpr (MODE == kModeL1) {
+#pragma unroll
+            for (int L = 1; L < K; ++L)
+#pragma unroll
+                for (int j = 0; j < C; ++j) {
+                    dold[L][j] = dmid[L][j];
+                    dmid[L][j] = odv[L][j];
+                }
+        }
     }
 
     __device__ __forceinline__ void run() {
@@ -578,10 +639,12 @@ struct SweepWarp {
                                         sbase + (uint32_t)(t & (kRS - 1)) * kRowBytes};
                 levels<1, false>(t, R4, r0, sptr);
                 store<1, false>(t, R4, sptr);
+                shift_duals();
             } else {
                 const uint32_t r0[3] = {0, 0, 0};
                 levels<1, true>(t, R4, r0, sptr);
                 store<1, true>(t, R4, sptr);
+                shift_duals();
                 if constexpr (K > 1) {
                     if (border) {
                         __syncwarp();
@@ -595,7 +658,10 @@ struct SweepWarp {
 };
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const SweepParams p) {
+// The solver modes carry f (and the dual FIFO): 3 blocks/SM = 168 registers,
+// no spills at K = 3.
+__global__ void __launch_bounds__(kThreads, MODE >= kModeL2 ? 3 : CF_MINB)
+    wmc_sweeps_kernel(const SweepParams p) {
     constexpr bool MAP = MODE == kModeMap;
     using G = Geo<K>;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -630,7 +696,9 @@ __global__ void __launch_bounds__(kThreads, CF_MINB) wmc_sweeps_kernel(const Swe
     if (sw.ys >= sw.ye) return;
     sw.srcp = p.src + (int64_t)plane * p.src_plane;
     sw.dstp = p.dst + (int64_t)plane * p.dst_plane;
-    sw.fp = MODE == kModeL2 ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
+    sw.fp = (MODE == kModeL2 || MODE == kModeL1) ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
+    sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
+    sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K>();
     sw.lbase = sw.sbase + 8 * C * sw.lane;

@@ -8,6 +8,8 @@ The reference (arXiv 1903.07189; /root/reference/SPEC.md) defines, in namespace
 * ``FlowConfig{dt, iters, scheme}``                      SPEC.md:250-253
 * ``kernel(name)`` / ``KernelBank`` (h1..h8)              SPEC.md:96-111
 * ``split_channels`` / ``merge_channels``                 SPEC.md:62-69
+* ``solve_l2_area`` / ``solve_l1_area`` / ``SolverConfig`` / ``SolveReport``
+                                                          SPEC.md:286-311
 
 Same names, argument meaning and error behaviour here; the arithmetic runs in
 the sm_100a kernels of ``libcurveflow_b200.so`` through the C-ABI
@@ -33,7 +35,7 @@ __all__ = [
     "FlowConfig", "FlowError", "wmc_half_laplace", "mc_flow", "mc_flow_u8", "kernel",
     "kernel_bank", "split_channels", "merge_channels", "synth_image", "sweeps_band",
     "mc_flow_image8", "wmc_energy", "wmc_histogram", "SolverConfig", "SolveReport", "solve_l2_area",
-    "max_sweeps_per_launch", "workspace_bytes",
+    "solve_l1_area", "solve", "data_fidelity", "max_sweeps_per_launch", "workspace_bytes",
 ]
 
 _HALF = ("h1", "h2", "h3", "h4", "h5", "h6", "h7", "h8")
@@ -230,63 +232,179 @@ def mc_flow_image8(img, cfg: FlowConfig, *, check_finite: bool = True):
     return out.cpu().numpy() if host else out
 
 
-@dataclass(frozen=True)
+@dataclass
 class SolverConfig:
-    """SPEC.md:286-289 (the fields the l2_area model uses; operator A = identity)."""
+    """SPEC.md:286-289 with operator A = identity.  model: "l2_area" (Eq. 30)
+    or "l1_area" (Eqs. 32-38).  report=True runs iteration by iteration and
+    fills the SolveReport series, stopping early once the relative update
+    ||U^{t+1} - U^t|| / ||U^t|| drops below 1e-6; report=False
+    fuses up to three iterations per launch and returns the final state."""
 
     lam: float = 0.0
     dt: float = 0.15
     iters: int = 500
     model: str = "l2_area"
+    alpha: float = 1.0
+    report: bool = False
 
     def validate(self) -> None:
-        if self.model != "l2_area":
-            raise NotImplementedError("only model='l2_area' (SPEC.md:296) is built on the "
-                                      "B200 path; l1_area / l2_epstv are out of scope this round")
+        if self.model not in ("l2_area", "l1_area"):
+            raise NotImplementedError(
+                f"model={self.model!r}: only 'l2_area' (SPEC.md:296) and 'l1_area' (SPEC.md:304) "
+                "run on the B200 WMC path; the eps-TV baseline solver is out of scope")
         if not (self.dt > 0.0) or not np.isfinite(self.dt):
             raise ValueError("SolverConfig.dt must be > 0")
         if not (self.lam >= 0.0) or not np.isfinite(self.lam):
             raise ValueError("SolverConfig.lam must be >= 0")
+        if not (self.alpha > 0.0) or not (self.alpha <= 1e30):
+            raise ValueError("SolverConfig.alpha must satisfy 0 < alpha <= 1e30 (SPEC.md:288)")
         if int(self.iters) != self.iters or self.iters < 0:
             raise ValueError("SolverConfig.iters must be a nonnegative integer")
 
 
 @dataclass
 class SolveReport:
-    """SPEC.md:290-293 subset: the final image, iterations run, and the final
-    data fidelity 0.5*||U - f||^2 (double)."""
+    """SPEC.md:290-293.  fidelity: final data term (l2: 0.5*||U - f||^2,
+    l1: ||U - f||_1, fp64).  With SolverConfig.report the per-iteration series
+    (fidelity, regularization = sum |H^w(U)|, total = fidelity + lam * reg)
+    have one entry per iteration run and `converged` says whether the
+    relative update fell below 1e-6; otherwise they are None.  dual: the
+    final d of the l1 model (None for l2)."""
 
     image: object
     iters: int
     fidelity: float
+    fidelity_series: list | None = None
+    regularization_series: list | None = None
+    total_series: list | None = None
+    converged: bool | None = None
+    dual: object = None
+
+
+CONVERGED_REL_UPDATE = 1e-6  # SPEC.md:292
+
+
+def _fidelity_dev(torch, u3, f3, q: float) -> float:
+    P, H, W = u3.shape
+    nbytes = int(lib().cf_wmc_reduce_workspace_bytes(W, H, P))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=u3.device)
+    out = torch.empty(1, dtype=torch.float64, device=u3.device)
+    check(lib().cf_wmc_fidelity_f64(u3.data_ptr(), None if f3 is None else f3.data_ptr(), W, H,
+                                    W, P, H * W, float(q), out.data_ptr(), ws.data_ptr(), nbytes,
+                                    _stream_ptr(torch, u3.device)), "fidelity")
+    return float(out.item())
+
+
+def data_fidelity(u, f=None, q: float = 1.0) -> float:
+    """sum |u - f|^q (f None: sum |u|^q), fp64, fixed order (csrc/wmc_reduce.cu)."""
+    torch = _torch()
+    a, _ = _device_image(u)
+    a3, _ = _as_planes(a.contiguous())
+    b3 = None
+    if f is not None:
+        b, _ = _device_image(f)
+        b3, _ = _as_planes(b.contiguous())
+        if b3.shape != a3.shape:
+            raise ValueError("u and f must have the same shape")
+    with torch.cuda.device(a3.device):
+        return _fidelity_dev(torch, a3, b3, q)
+
+
+def _solve(f, cfg: SolverConfig, model: str) -> SolveReport:
+    torch = _torch()
+    cfg.validate()
+    if cfg.model != model:
+        raise ValueError(f"cfg.model must be {model!r}")
+    src, host = _device_image(f)
+    f3, squeeze = _as_planes(src.contiguous())
+    P, H, W = f3.shape
+    l1 = model == "l1_area"
+    u = torch.empty_like(f3)
+    d = torch.empty_like(f3) if l1 else None
+    nbytes = int(lib().cf_wmc_solve_l1_area_workspace_bytes(W, H, W, P, H * W) if l1
+                 else lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=f3.device)
+    bad = C.c_int32(0)
+    q = 1.0 if l1 else 2.0
+    scale = 1.0 if l1 else 0.5
+
+    def step(iters: int, init: bool) -> None:
+        strm = _stream_ptr(torch, f3.device)
+        if l1:
+            rc = lib().cf_wmc_solve_l1_area_f32(f3.data_ptr(), u.data_ptr(), d.data_ptr(), W, H,
+                                                W, P, H * W, int(iters), float(cfg.dt),
+                                                float(cfg.lam), float(cfg.alpha), int(init),
+                                                ws.data_ptr(), nbytes, C.byref(bad), strm)
+        else:
+            rc = lib().cf_wmc_solve_l2_area_f32(f3.data_ptr(), u.data_ptr(), W, H, W, P, H * W,
+                                                int(iters), float(cfg.dt), float(cfg.lam),
+                                                int(init), ws.data_ptr(), nbytes, C.byref(bad),
+                                                strm)
+        if rc == CF_ENONFINITE:
+            raise FlowError(done + bad.value)
+        check(rc, "solve_" + model)
+
+    done = 0
+    fid_s = reg_s = tot_s = None
+    converged = None
+    with torch.cuda.device(f3.device):
+        if not cfg.report:
+            step(int(cfg.iters), True)
+            done = int(cfg.iters)
+        else:
+            fid_s, reg_s, tot_s = [], [], []
+            converged = False
+            step(0, True)                     # U^0 = f (, d^0 = 0)
+            prev = u.clone()
+            for _ in range(int(cfg.iters)):
+                step(1, False)
+                done += 1
+                fid = scale * _fidelity_dev(torch, u, f3, q)
+                reg = wmc_energy(u, 1.0)
+                fid_s.append(fid)
+                reg_s.append(reg)
+                tot_s.append(fid + cfg.lam * reg)
+                num = _fidelity_dev(torch, u, prev, 2.0)
+                den = _fidelity_dev(torch, prev, None, 2.0)
+                rel = float(np.sqrt(num) / max(np.sqrt(den), np.finfo(np.float64).tiny))
+                if rel < CONVERGED_REL_UPDATE:
+                    converged = True
+                    break
+                prev.copy_(u)
+        fidelity = scale * _fidelity_dev(torch, u, f3, q)
+
+    def out(t):
+        if t is None:
+            return None
+        r = t[0] if squeeze else t
+        if host:
+            r = r.cpu().numpy() if isinstance(f, np.ndarray) else r.cpu()
+        return r
+
+    return SolveReport(image=out(u), iters=done, fidelity=fidelity, fidelity_series=fid_s,
+                       regularization_series=reg_s, total_series=tot_s, converged=converged,
+                       dual=out(d))
 
 
 def solve_l2_area(f, cfg: SolverConfig) -> SolveReport:
     """solve_l2_area (SPEC.md:296-303, A = I): U^0 = f,
     U <- U + dt*((f - U) + lam*H^w(U)); raises FlowError(iteration) on a
     non-finite iterate."""
-    torch = _torch()
+    return _solve(f, cfg, "l2_area")
+
+
+def solve_l1_area(f, cfg: SolverConfig) -> SolveReport:
+    """solve_l1_area (A = I): U^0 = f, d^0 = 0; per iteration
+    r = U - f + d, d' = clamp(r, -alpha, alpha),
+    U <- U + dt*(lam*H^w(U) - (2d' - d)/alpha); raises
+    FlowError(iteration) on divergence."""
+    return _solve(f, cfg, "l1_area")
+
+
+def solve(f, cfg: SolverConfig) -> SolveReport:
+    """Dispatch on cfg.model."""
     cfg.validate()
-    src, host = _device_image(f)
-    f3, squeeze = _as_planes(src.contiguous())
-    P, H, W = f3.shape
-    u = torch.empty_like(f3)
-    nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
-    ws = torch.empty(nbytes, dtype=torch.uint8, device=f3.device)
-    bad = C.c_int32(0)
-    with torch.cuda.device(f3.device):
-        rc = lib().cf_wmc_solve_l2_area_f32(f3.data_ptr(), u.data_ptr(), W, H, W, P, H * W,
-                                            int(cfg.iters), float(cfg.dt), float(cfg.lam),
-                                            ws.data_ptr(), nbytes, C.byref(bad),
-                                            _stream_ptr(torch, f3.device))
-    if rc == CF_ENONFINITE:
-        raise FlowError(bad.value)
-    check(rc, "solve_l2_area")
-    fid = float(0.5 * ((u.double() - f3.double()) ** 2).sum().item())
-    res = u[0] if squeeze else u
-    if host:
-        res = res.cpu().numpy() if isinstance(f, np.ndarray) else res.cpu()
-    return SolveReport(image=res, iters=int(cfg.iters), fidelity=fid)
+    return _solve(f, cfg, cfg.model)
 
 
 def wmc_energy(img, q: float = 1.0) -> float:

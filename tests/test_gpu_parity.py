@@ -153,6 +153,19 @@ def test_cpp_cli_matches_oracle():
     out = json.loads(subprocess.run([exe, "op", "--size", str(H), str(W), "--seed", "3"],
                                     capture_output=True, text=True, check=True).stdout)
     assert out["fnv1a"] == fnv(oracle.wmc_map_f32(img))
+    # smooth through curveflow::cuda::solve
+    for model in ("l1", "l2"):
+        out = json.loads(subprocess.run(
+            [exe, "smooth", "--size", str(H), str(W), "--seed", "3", "--iters", "8", "--model",
+             model, "--lambda", "2.5", "--alpha", "0.25"],
+            capture_output=True, text=True, check=True).stdout)
+        if model == "l1":
+            ref, _, _ = oracle.solve_l1_area_f32(img, 8, 0.15, 2.5, 0.25)
+            assert out["fidelity"] == oracle.fidelity(ref, img, 1.0)
+        else:
+            ref, _ = oracle.solve_l2_area_f32(img, 8, 0.15, 2.5)
+            assert out["fidelity"] == 0.5 * oracle.fidelity(ref, img, 2.0)
+        assert out["fnv1a"] == fnv(ref), model
 
 
 @pytest.mark.parametrize("scale", [1e-38, 1e-30, 255.0, 1e6])
@@ -195,6 +208,78 @@ def test_solve_l2_area_bitexact(lam, dt, iters):
     assert_bitexact(rep.image.cpu().numpy(), ref, f"l2 lam={lam} iters={iters}")
     if lam == 0.0:
         assert_bitexact(rep.image.cpu().numpy(), f, "lambda=0 fixed point")
+
+
+@pytest.mark.parametrize("shape,lam,alpha,dt,iters", [
+    ((53, 140), 3.0, 0.2, 0.15, 1), ((53, 140), 3.0, 0.2, 0.15, 2), ((53, 140), 3.0, 0.2, 0.15, 7),
+    ((67, 131), 0.5, 0.05, 0.15, 12), ((130, 257), 10.0, 1.0, 0.05, 9), ((5, 300), 2.0, 0.3, 0.15, 4),
+    ((1, 1), 1.0, 1.0, 0.15, 3), ((300, 3), 2.0, 0.5, 0.15, 5)])
+def test_solve_l1_area_bitexact(shape, lam, alpha, dt, iters):
+    """solve_l1_area: U and the dual d bit-exact vs the
+    fp32 canonical oracle for every launch schedule (fused levels carry d)."""
+    h, w = shape
+    f = np.stack([cf.synth_image(h, w, seed=70 + s, n_rects=5, n_discs=5, sigma=0.1)
+                  for s in range(2)])
+    rep = cf.solve_l1_area(torch.from_numpy(f).cuda(),
+                           cf.SolverConfig(model="l1_area", lam=lam, alpha=alpha, dt=dt,
+                                           iters=iters))
+    ref_u, ref_d, bad = oracle.solve_l1_area_f32(f, iters, dt, lam, alpha)
+    assert bad == 0 and rep.iters == iters
+    assert_bitexact(rep.image.cpu().numpy(), ref_u, f"l1 U {shape} iters={iters}")
+    assert_bitexact(rep.dual.cpu().numpy(), ref_d, f"l1 d {shape} iters={iters}")
+    assert rep.fidelity == oracle.fidelity(ref_u, f, 1.0)
+
+
+def test_solve_l1_area_lambda0_and_divergence():
+    f = cf.synth_image(45, 77, seed=3, n_rects=4, n_discs=4, sigma=0.1)
+    rep = cf.solve_l1_area(f, cf.SolverConfig(model="l1_area", lam=0.0, alpha=0.3, iters=11))
+    assert_bitexact(rep.image, f, "l1 lambda=0 fixed point")
+    assert not np.any(rep.dual)
+    _, _, bad = oracle.solve_l1_area_f32(f, 400, 0.15, 20.0, 1.0)
+    assert bad > 0
+    with pytest.raises(cf.FlowError) as e:
+        cf.solve_l1_area(f, cf.SolverConfig(model="l1_area", lam=20.0, alpha=1.0, iters=400))
+    assert e.value.iteration == bad
+
+
+@pytest.mark.parametrize("model", ["l1_area", "l2_area"])
+def test_solver_report_series(model):
+    """SolveReport series: one entry per iteration run,
+    fidelity / regularization equal to the oracle's fixed-order sums of the
+    oracle's iterates; convergence stop when the relative update < 1e-6."""
+    f = cf.synth_image(40, 72, seed=21, n_rects=4, n_discs=4, sigma=0.1)
+    lam, alpha, dt, iters = 2.0, 0.2, 0.15, 6
+    rep = cf.solve(f, cf.SolverConfig(model=model, lam=lam, alpha=alpha, dt=dt, iters=iters,
+                                      report=True))
+    assert rep.iters == iters and len(rep.fidelity_series) == iters
+    assert len(rep.regularization_series) == iters and rep.converged is False
+    state = None
+    for t in range(iters):
+        if model == "l1_area":
+            u, d, _ = oracle.solve_l1_area_f32(f, 1, dt, lam, alpha, state=state)
+            state = (u, d)
+            fid = oracle.fidelity(u, f, 1.0)
+        else:
+            u, _ = oracle.solve_l2_area_f32(f, 1, dt, lam, u0=state)
+            state = u
+            fid = 0.5 * oracle.fidelity(u, f, 2.0)
+        assert rep.fidelity_series[t] == fid, t
+        assert rep.regularization_series[t] == oracle.wmc_energy(u, 1.0), t
+        assert rep.total_series[t] == fid + lam * oracle.wmc_energy(u, 1.0)
+    assert_bitexact(rep.image, u, f"{model} report final image")
+    # lambda = 0 l2: the first update is exactly zero -> converged after 1 iteration
+    rep0 = cf.solve(f, cf.SolverConfig(model="l2_area", lam=0.0, iters=50, report=True))
+    assert rep0.converged is True and rep0.iters == 1
+
+
+def test_data_fidelity_bitexact():
+    rng = np.random.default_rng(5)
+    u = rng.normal(0, 1, (3, 41, 97)).astype(np.float32)
+    f = rng.normal(0, 1, (3, 41, 97)).astype(np.float32)
+    for q in (1.0, 2.0, 0.5):
+        assert cf.data_fidelity(torch.from_numpy(u).cuda(), torch.from_numpy(f).cuda(), q) == \
+            oracle.fidelity(u, f, q)
+    assert cf.data_fidelity(u, None, 2.0) == oracle.fidelity(u, None, 2.0)
 
 
 @pytest.mark.parametrize("q", [1.0, 2.0, 0.5])

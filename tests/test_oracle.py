@@ -330,6 +330,122 @@ def test_l2_area_smooths_toward_data():
     assert lap(u).var() < 0.5 * lap(f).var()
 
 
+# ------------------------------------------------------- solve_l1_area -----
+@pytest.mark.parametrize("r,alpha,b,d", [(0.5, 0.3, 0.2, 0.3), (-0.5, 0.3, -0.2, -0.3),
+                                         (0.2, 0.3, 0.0, 0.2), (0.1, 0.3, 0.0, 0.1)])
+def test_l1_shrinkage_and_dual_kats(r, alpha, b, d):
+    """Eq. 36 shrinkage and Eq. 37 dual clamp branches
+    (fp32: b is fl(r -/+ alpha))."""
+    gb, gd = oracle.l1_px(r, alpha)
+    f32 = np.float32
+    assert gd == f32(d)
+    if b > 0:
+        assert gb == f32(f32(r) - f32(alpha))
+    elif b < 0:
+        assert gb == f32(f32(r) + f32(alpha))
+    else:
+        assert gb == 0.0
+    assert abs(gb - b) < 1e-7
+
+
+def test_l1_identity_b_equals_r_minus_dnew():
+    """b - (r - d_new) = 0 for every pixel (bitwise in fp32)."""
+    rng = np.random.default_rng(11)
+    for r, a in zip(rng.normal(0, 1, 2000).astype(np.float32),
+                    rng.uniform(0.01, 2, 2000).astype(np.float32)):
+        b, d = oracle.l1_px(float(r), float(a))
+        assert np.float32(b) == np.float32(np.float32(r) - np.float32(d))
+
+
+def _l1_numpy_step(u, d, f, dt, lam, alpha):
+    """Independent numpy restatement of one l1 iteration."""
+    f32 = np.float32
+    hw = oracle.wmc_flowmap_f32(u)
+    r = (u - f) + d                                   # fl(fl(u - f) + d)
+    dn = np.minimum(np.maximum(r, f32(-alpha)), f32(alpha))
+    e = (dn + dn) - d                                 # 2d' exact, one rounding
+    q = e * f32(-(f32(1.0) / f32(alpha)))
+    s = (f32(lam) * hw.astype(np.float64) + q.astype(np.float64)).astype(np.float32)
+    un = (f32(dt) * s.astype(np.float64) + u.astype(np.float64)).astype(np.float32)
+    return un, dn
+
+
+def test_l1_area_matches_numpy_restatement():
+    f = cf.synth_image(29, 37, seed=12, n_rects=3, n_discs=3, sigma=0.1)
+    dt, lam, alpha = 0.15, 2.0, 0.05
+    u, d = f.copy(), np.zeros_like(f)
+    for _ in range(6):
+        u, d = _l1_numpy_step(u, d, f, dt, lam, alpha)
+    gu, gd, bad = oracle.solve_l1_area_f32(f, 6, dt, lam, alpha)
+    assert bad == 0
+    assert np.max(np.abs(gu - u)) <= 1e-6 and np.array_equal(gd, d)
+
+
+def test_l1_area_lambda0_is_fixed_point():
+    """U^0 = f, d^0 = 0 is a fixed point at lambda = 0 (r = 0 -> d' = 0)."""
+    f = cf.synth_image(23, 31, seed=5, n_rects=3, n_discs=3, sigma=0.1)
+    u, d, bad = oracle.solve_l1_area_f32(f, 17, 0.15, 0.0, 0.3)
+    assert bad == 0 and np.array_equal(u.view(np.uint32), f.view(np.uint32))
+    assert not np.any(d)
+
+
+def test_l1_area_continue_equals_single_run():
+    f = cf.synth_image(21, 33, seed=8, n_rects=3, n_discs=3, sigma=0.1)
+    u7, d7, _ = oracle.solve_l1_area_f32(f, 7, 0.15, 3.0, 0.2)
+    u3, d3, _ = oracle.solve_l1_area_f32(f, 3, 0.15, 3.0, 0.2)
+    u, d, _ = oracle.solve_l1_area_f32(f, 4, 0.15, 3.0, 0.2, state=(u3, d3))
+    assert np.array_equal(u.view(np.uint32), u7.view(np.uint32))
+    assert np.array_equal(d.view(np.uint32), d7.view(np.uint32))
+    u2, _ = oracle.solve_l2_area_f32(f, 3, 0.15, 3.0)
+    u2b, _ = oracle.solve_l2_area_f32(f, 4, 0.15, 3.0, u0=u2)
+    u2c, _ = oracle.solve_l2_area_f32(f, 7, 0.15, 3.0)
+    assert np.array_equal(u2b.view(np.uint32), u2c.view(np.uint32))
+
+
+def _ssim(a, b):
+    """Mean SSIM over 8x8 windows at stride 4 ([0,1] data range)."""
+    from numpy.lib.stride_tricks import sliding_window_view as sw
+    a, b = a.astype(np.float64), b.astype(np.float64)
+    c1, c2 = 0.01 ** 2, 0.03 ** 2
+    A, B = sw(a, (8, 8))[::4, ::4], sw(b, (8, 8))[::4, ::4]
+    ma, mb = A.mean((-1, -2)), B.mean((-1, -2))
+    va, vb = A.var((-1, -2)), B.var((-1, -2))
+    cov = ((A - ma[..., None, None]) * (B - mb[..., None, None])).mean((-1, -2))
+    return float((((2 * ma * mb + c1) * (2 * cov + c2)) /
+                  ((ma ** 2 + mb ** 2 + c1) * (va + vb + c2))).mean())
+
+
+def test_l1_area_lambda_sweep_ssim_monotone():
+    """SPEC.md:311: SSIM(f, U*) non-increasing over lambda in {1, 3, 10, 20}
+    on a 256^2 image (synthetic phantom; dt = 0.04 keeps dt*lambda <= 0.8,
+    the flow's stable range -- at the default dt = 0.15, lambda = 20 diverges)."""
+    f = cf.synth_image(256, 256, seed=7, n_rects=6, n_discs=6, sigma=0.05)
+    vals = []
+    for lam in (1.0, 3.0, 10.0, 20.0):
+        u, _, bad = oracle.solve_l1_area_f32(f, 500, 0.04, lam, 1.0)
+        assert bad == 0
+        vals.append(_ssim(f, u))
+    assert all(x >= y for x, y in zip(vals, vals[1:])), vals
+    assert vals[-1] < vals[0]
+
+
+def test_l1_area_divergence_reports_iteration():
+    f = cf.synth_image(64, 64, seed=9, n_rects=4, n_discs=4, sigma=0.1)
+    _, _, bad = oracle.solve_l1_area_f32(f, 400, 0.15, 20.0, 1.0)
+    assert bad > 0
+
+
+def test_fidelity_fixed_order_sum():
+    rng = np.random.default_rng(3)
+    u = rng.normal(0, 1, (2, 37, 70)).astype(np.float32)
+    f = rng.normal(0, 1, (2, 37, 70)).astype(np.float32)
+    for q in (1.0, 2.0, 0.5, 1.7):
+        ref = np.sum(np.abs(u.astype(np.float64) - f) ** q)
+        assert abs(oracle.fidelity(u, f, q) - ref) <= 1e-12 * ref
+    assert oracle.fidelity(u, None, 2.0) == pytest.approx(np.sum(u.astype(np.float64) ** 2),
+                                                          rel=1e-13)
+
+
 # ------------------------------------------------- energies / histogram ----
 def test_wmc_energy_kats():
     """constant -> 0; WMC energy (q=1) is degree-1
