@@ -169,7 +169,7 @@ def bench_b200(args, cfg):
     sp = stream.cuda_stream
 
     # ---------------- inputs (host, pinned) and device buffers ----------------
-    K = 3  # sweeps per launch, = the C-ABI filter's schedule
+    K = int(L.cf_wmc_filter_sweeps_per_launch())  # = the C-ABI filter schedule
     if world > 1 and cfg.sharding == "rows":
         lay = sharded.BandLayout(cfg.h, cfg.w, rank, world, K)
         rows = (lay.r0, lay.r1)

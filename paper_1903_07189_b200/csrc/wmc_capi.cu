@@ -21,8 +21,11 @@
 namespace {
 
 constexpr int kMaxLevels = 4;            // max sweeps fused per launch (band API)
-constexpr int kFlowLevels = 3;           // sweeps per launch the filter schedules (measured
-                                         // fastest on B200, DESIGN.md §4 / profiles/)
+#ifndef CF_FLOW_LEVELS
+#define CF_FLOW_LEVELS 2
+#endif
+constexpr int kFlowLevels = CF_FLOW_LEVELS;  // sweeps per launch the filter schedules
+                                             // (measured fastest on B200)
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
 
@@ -201,6 +204,8 @@ CF_API const char* cf_status_string(int status) {
 CF_API int cf_last_cuda_error(void) { return g_last_cuda; }
 
 CF_API int32_t cf_wmc_max_sweeps_per_launch(void) { return kMaxLevels; }
+
+CF_API int32_t cf_wmc_filter_sweeps_per_launch(void) { return kFlowLevels; }
 
 CF_API int32_t cf_wmc_filter_launches(int32_t iters) {
     if (iters <= 0) return 0;

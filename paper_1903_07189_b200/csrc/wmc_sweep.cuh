@@ -45,8 +45,19 @@
 
 namespace cfk {
 
+#ifndef CF_FAST_UNROLL
+#define CF_FAST_UNROLL 2  // steady-state loop unroll (register renaming of the carries)
+#endif
+constexpr int kFastUnroll = CF_FAST_UNROLL;
+// Resident 128-thread blocks per SM the register budget targets (measured on
+// B200, 16384^2): K = 1, 3 and the map run best at 4 blocks
+// (128 registers, K = 3 with a small spill); K = 2, 4 at 3 blocks (168
+// registers, no spills; 4 blocks would spill and lose 16 %).
 #ifndef CF_MINB
-#define CF_MINB 4     // resident 128-thread blocks per SM the register budget targets
+#define CF_MINB 4
+#endif
+#ifndef CF_MINB_EVEN
+#define CF_MINB_EVEN 3
 #endif
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = 32 * kWarpsPerBlock;
@@ -607,60 +618,74 @@ struct SweepWarp {
         // level-K store row (t - lag(K), column xf[0])
         const float* lptr = srcp + (int64_t)(t_begin + kRD - P.src_row0) * P.src_pitch + xf[0];
         float* sptr = dstp + (int64_t)(t_begin - lag(K) - P.dst_row0) * P.dst_pitch + xf[0];
-        for (int t = t_begin; t <= t_end; ++t) {
-            cp_async_wait_rd();       // this lane's copies of row t landed
-            if (border) {
-                __syncwarp();
-                if (t < rhi(0)) clamp_row(row_addr<0>(t));
-            }
-            __syncwarp();             // rows of step t-1 and row t visible to all lanes
-            if (t + kRD < rhi(0)) {
-                if (!border) {
-                    const uint32_t sa =
-                        sbase + (uint32_t)((t + kRD) & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
-#pragma unroll
-                    for (int j = 0; j < C; ++j) {
-                        cp_async4(sa + 8 * j, lptr + j);
-                        cp_async4(sa + 8 * j + 4, lptr + G::S + j);
-                    }
-                } else {
-                    prefetch(t + kRD);
-                }
-            }
-            lptr += P.src_pitch;
-            cp_async_commit();
-            const uint32_t R4[4] = {(uint32_t)(t & 3) * kRowBytes,
-                                    (uint32_t)((t + 1) & 3) * kRowBytes,
-                                    (uint32_t)((t + 2) & 3) * kRowBytes,
-                                    (uint32_t)((t + 3) & 3) * kRowBytes};
-            if (t >= t_s && t <= t_e) {
-                const uint32_t r0[3] = {sbase + (uint32_t)((t - 2) & (kRS - 1)) * kRowBytes,
-                                        sbase + (uint32_t)((t - 1) & (kRS - 1)) * kRowBytes,
-                                        sbase + (uint32_t)(t & (kRS - 1)) * kRowBytes};
-                levels<1, false>(t, R4, r0, sptr);
-                store<1, false>(t, R4, sptr);
-                shift_duals();
-            } else {
-                const uint32_t r0[3] = {0, 0, 0};
-                levels<1, true>(t, R4, r0, sptr);
-                store<1, true>(t, R4, sptr);
-                shift_duals();
-                if constexpr (K > 1) {
-                    if (border) {
-                        __syncwarp();
-                        clamp_levels<1>(t);
-                    }
-                }
-            }
-            sptr += P.dst_pitch;
+        // Three loops -- checked prologue, fast steady state, checked
+        // epilogue -- so the steady-state loop's carried registers never
+        // join the checked path's (a per-step if/else costs ~5 register
+        // moves per pixel-update at the join).
+        const int f0 = min(t_s, t_end + 1), f1 = min(t_e, t_end);
+        int t = t_begin;
+        for (; t < f0; ++t) step<false>(t, lptr, sptr);
+#pragma unroll kFastUnroll
+        for (; t <= f1; ++t) step<true>(t, lptr, sptr);
+        for (; t <= t_end; ++t) step<false>(t, lptr, sptr);
+    }
+
+    template <bool FAST>
+    __device__ __forceinline__ void step(int t, const float*& lptr, float*& sptr) {
+        cp_async_wait_rd();       // this lane's copies of row t landed
+        if (!FAST && border) {
+            __syncwarp();
+            if (t < rhi(0)) clamp_row(row_addr<0>(t));
         }
+        __syncwarp();             // rows of step t-1 and row t visible to all lanes
+        if (t + kRD < rhi(0)) {
+            if (FAST || !border) {
+                const uint32_t sa =
+                    sbase + (uint32_t)((t + kRD) & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
+#pragma unroll
+                for (int j = 0; j < C; ++j) {
+                    cp_async4(sa + 8 * j, lptr + j);
+                    cp_async4(sa + 8 * j + 4, lptr + G::S + j);
+                }
+            } else {
+                prefetch(t + kRD);
+            }
+        }
+        lptr += P.src_pitch;
+        cp_async_commit();
+        const uint32_t R4[4] = {(uint32_t)(t & 3) * kRowBytes,
+                                (uint32_t)((t + 1) & 3) * kRowBytes,
+                                (uint32_t)((t + 2) & 3) * kRowBytes,
+                                (uint32_t)((t + 3) & 3) * kRowBytes};
+        if constexpr (FAST) {
+            const uint32_t r0[3] = {sbase + (uint32_t)((t - 2) & (kRS - 1)) * kRowBytes,
+                                    sbase + (uint32_t)((t - 1) & (kRS - 1)) * kRowBytes,
+                                    sbase + (uint32_t)(t & (kRS - 1)) * kRowBytes};
+            levels<1, false>(t, R4, r0, sptr);
+            store<1, false>(t, R4, sptr);
+            shift_duals();
+        } else {
+            const uint32_t r0[3] = {0, 0, 0};
+            levels<1, true>(t, R4, r0, sptr);
+            store<1, true>(t, R4, sptr);
+            shift_duals();
+            if constexpr (K > 1) {
+                if (border) {
+                    __syncwarp();
+                    clamp_levels<1>(t);
+                }
+            }
+        }
+        sptr += P.dst_pitch;
     }
 };
 
 template <int K, int MODE>
 // The solver modes carry f (and the dual FIFO): 3 blocks/SM = 168 registers,
 // no spills at K = 3.
-__global__ void __launch_bounds__(kThreads, MODE >= kModeL2 ? 3 : CF_MINB)
+__global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
+                                           : (MODE == kModeFlow && K % 2 == 0) ? CF_MINB_EVEN
+                                                                               : CF_MINB)
     wmc_sweeps_kernel(const SweepParams p) {
     constexpr bool MAP = MODE == kModeMap;
     using G = Geo<K>;
