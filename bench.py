@@ -33,6 +33,19 @@ sys.path.insert(0, ROOT)
 METRIC = "WMC Gpixel-updates/s"
 UNIT = "Gpixel-updates/s"
 BYTES_PER_UPDATE = 8  # 4 B read of U^t + 4 B write of U^{t+1}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def ncu_traffic(kernel: str, h: int, w: int, planes: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at
+    this geometry, from the committed ncu --set full capture
+    (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(f"{kernel}@{planes}x{h}x{w}")
+    except Exception:
+        return None
 
 
 def peaks():
@@ -190,11 +203,16 @@ def bench_b200(args, cfg):
     updates_local = n_px_local * max(1, cfg.iters)
     launches_per_step = 0
 
+    def cur_sp():  # the current stream (a graph's capture stream while capturing)
+        return torch.cuda.current_stream(dev).cuda_stream
+
+    ws = None
     if cfg.iters == 0:  # single map evaluation (cfg1)
         out = torch.empty(dev_in.shape, dtype=torch.float32, device=dev)
 
         def step():
-            cf.lib().cf_wmc_map_f32(dev_in.data_ptr(), out.data_ptr(), W, H, W, P, H * W, sp)
+            rc = L.cf_wmc_map_f32(dev_in.data_ptr(), out.data_ptr(), W, H, W, P, H * W, cur_sp())
+            assert rc == 0, rc
         launches_per_step = 1
     elif world > 1 and cfg.sharding == "rows":
         buf_a = torch.zeros((lay.rows, cfg.w), dtype=torch.float32, device=dev)
@@ -211,19 +229,19 @@ def bench_b200(args, cfg):
         work = torch.empty(dev_in.shape, dtype=torch.float32, device=dev)
         nbytes = int(L.cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
         ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        import ctypes
-        bad = ctypes.c_int32(0)
+        # first_bad_iter = NULL: no host sync inside the step (capturable);
+        # the device flag is checked once after the timed region.
         if cfg.u8:
             def step():
                 rc = L.cf_wmc_filter_u8_f32(dev_in.data_ptr(), W, H * W, work.data_ptr(), W, H,
                                             W, P, H * W, cfg.iters, cfg.dt, ws.data_ptr(),
-                                            nbytes, ctypes.byref(bad), sp)
+                                            nbytes, None, cur_sp())
                 assert rc == 0, rc
         else:
             def step():
                 work.copy_(dev_in)  # the filter is in place; restore U^0 each step
                 rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, cfg.iters, cfg.dt,
-                                         ws.data_ptr(), nbytes, ctypes.byref(bad), sp)
+                                         ws.data_ptr(), nbytes, None, cur_sp())
                 assert rc == 0, rc
         launches_per_step = int(L.cf_wmc_filter_launches(cfg.iters))
 
@@ -232,15 +250,24 @@ def bench_b200(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    # L2 rule: a working set that fits in L2 (126 MB) is flushed between timed
+    # steps (a 256 MiB memset, outside the per-step events).
+    l2_resident = n_px_local * 4 <= L2_BYTES
+    flush_buf = (torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+                 if l2_resident else None)
+
     def timed(fn, steps):
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        for e0, e1 in evs:
+            if flush_buf is not None:
+                flush_buf.zero_()
+            e0.record(stream)
             fn()
-        e1.record(stream)
+            e1.record(stream)
         barrier()
-        ms = e0.elapsed_time(e1)
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
         if world > 1:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -250,8 +277,23 @@ def bench_b200(args, cfg):
     # ---------------- device-resident timing (value) ----------------
     for _ in range(args.warmup):
         step()
+    torch.cuda.synchronize(dev)
+    run_step = step
+    graph = world == 1  # one CUDA graph per step: no host launch gaps in the timed region
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        run_step = g.replay
     with ClockSampler(local) as clk:
-        ms_step = timed(step, args.steps)
+        ms_step = timed(run_step, args.steps)
+    if ws is not None:  # device non-finite flag of the last timed step
+        import ctypes
+        bad = ctypes.c_int32(0)
+        rc = L.cf_wmc_filter_query_nonfinite(ws.data_ptr(), ctypes.byref(bad), sp)
+        assert rc == 0, f"non-finite value in the timed run (iteration {bad.value})"
     updates_job = cfg.updates  # whole job over all ranks (strong scaling for rows)
     if world > 1 and cfg.sharding == "images":
         updates_job = updates_local * world  # per-rank fixed share (weak scaling)
@@ -384,8 +426,10 @@ def bench_b200(args, cfg):
             "sweeps_per_launch": 1 if cfg.iters == 0 else K,
             "parallelism": (f"rowband{world}" if cfg.sharding == "rows" and world > 1 else
                             f"images{world}" if world > 1 else "single"),
-            "l2": "inputs larger than L2 (126 MB)" if n_px_local * 4 > 126e6 else
-                  "L2-resident working set (no flush; flagged)",
+            "l2": ("inputs larger than L2 (126 MB)" if not l2_resident else
+                   "working set fits in L2: 256 MiB flush between timed steps"),
+            "timing": ("one CUDA graph per step, CUDA events per step" if graph else
+                       "CUDA events around the step loop, max over ranks"),
         },
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4),
@@ -403,8 +447,9 @@ def bench_b200(args, cfg):
             "kernel": f"wmc_sweeps_kernel<K={K}>" if cfg.iters else "wmc_sweeps_kernel<MAP>",
             "kernel_ms": round(kern_ms, 4), "peak_source": peak_src,
             "note": "algorithmic 8 B per pixel-update x updates per launch / launch time; "
-                    "physical DRAM bytes per launch are in profiles/ (ncu)",
+                    "traffic: physical DRAM bytes per launch from the committed ncu capture",
         }
+        res["roofline"]["traffic"] = ncu_traffic(res["roofline"]["kernel"], H, W, P)
     if world == 1 and not args.no_cpu_baseline:
         rate, cores, sample, kind = cpu_reference_sample(cfg, host[0] if host.ndim == 3 else host)
         res["cpu_baseline"] = {"value": round(rate, 4), "unit": UNIT, "cores": cores,
