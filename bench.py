@@ -182,7 +182,8 @@ def bench_b200(args, cfg):
     sp = stream.cuda_stream
 
     # ---------------- inputs (host, pinned) and device buffers ----------------
-    K = int(L.cf_wmc_filter_sweeps_per_launch())  # = the C-ABI filter schedule
+    # sweeps per launch = the C-ABI filter's schedule for this geometry
+    K = int(L.cf_wmc_filter_sweeps_per_launch(cfg.w, cfg.h, cfg.planes))
     if world > 1 and cfg.sharding == "rows":
         lay = sharded.BandLayout(cfg.h, cfg.w, rank, world, K)
         rows = (lay.r0, lay.r1)
@@ -243,7 +244,7 @@ def bench_b200(args, cfg):
                 rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, cfg.iters, cfg.dt,
                                          ws.data_ptr(), nbytes, None, cur_sp())
                 assert rc == 0, rc
-        launches_per_step = int(L.cf_wmc_filter_launches(cfg.iters))
+        launches_per_step = int(L.cf_wmc_filter_launches(W, H, P, cfg.iters))
 
     def barrier():
         if world > 1:

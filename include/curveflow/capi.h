@@ -147,10 +147,11 @@ CF_API int cf_wmc_solve_l1_area_f32(const float* f, float* u, float* d, int32_t 
 /* atomically min-ed with the first iteration producing a non-finite value.*/
 /* ---------------------------------------------------------------------- */
 CF_API int32_t cf_wmc_max_sweeps_per_launch(void);
-/* Number of kernel launches cf_wmc_filter_f32 / _u8_f32 enqueue for iters, */
-/* and the sweeps fused per launch they schedule (at most).                 */
-CF_API int32_t cf_wmc_filter_launches(int32_t iters);
-CF_API int32_t cf_wmc_filter_sweeps_per_launch(void);
+/* Number of kernel launches cf_wmc_filter_f32 / _u8_f32 (and the solvers) */
+/* enqueue for iters on a w x h x planes image, and the sweeps fused per    */
+/* launch they schedule (at most; 2 up to 4 Mi pixels, else 3).             */
+CF_API int32_t cf_wmc_filter_launches(int32_t w, int32_t h, int32_t planes, int32_t iters);
+CF_API int32_t cf_wmc_filter_sweeps_per_launch(int32_t w, int32_t h, int32_t planes);
 CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,
                                   float* dst, int32_t dst_row0, int32_t w, int32_t h,
                                   int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,

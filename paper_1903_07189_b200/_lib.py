@@ -45,8 +45,8 @@ SIGNATURES = {
     "cf_wmc_solve_l1_area_f32": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32,
                                            _f32, _f32, _f32, _i32, _vp, _sz, _pi32, _vp]),
     "cf_wmc_max_sweeps_per_launch": (_i32, []),
-    "cf_wmc_filter_launches": (_i32, [_i32]),
-    "cf_wmc_filter_sweeps_per_launch": (_i32, []),
+    "cf_wmc_filter_launches": (_i32, [_i32, _i32, _i32, _i32]),
+    "cf_wmc_filter_sweeps_per_launch": (_i32, [_i32, _i32, _i32]),
     "cf_wmc_sweeps_band_f32": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i32,
                                          _i32, _i32, _f32, _i32, _vp, _vp]),
     "cf_image8_to_planes_f32": (C.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _vp]),

@@ -21,11 +21,12 @@
 namespace {
 
 constexpr int kMaxLevels = 4;            // max sweeps fused per launch (band API)
-#ifndef CF_FLOW_LEVELS
-#define CF_FLOW_LEVELS 2
-#endif
-constexpr int kFlowLevels = CF_FLOW_LEVELS;  // sweeps per launch the filter schedules
-                                             // (measured fastest on B200)
+// Sweeps per launch the filter schedules (measured on B200):
+// 3 for large working sets (cfg3-5: +8-15 % over 2), 2 up to kSmallPixels
+// pixels (cfg2: L2-resident, few warp tasks -- +29 % over 3).
+constexpr int kFlowLevelsLarge = 3;
+constexpr int kFlowLevelsSmall = 2;
+constexpr int64_t kSmallPixels = 4 << 20;
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
 
@@ -147,13 +148,17 @@ bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane
     return true;
 }
 
-// Launch schedule: sweeps per launch, at most kFlowLevels each, an EVEN number
+int flow_levels(int32_t w, int32_t h, int32_t planes) {
+    return (int64_t)w * h * planes <= kSmallPixels ? kFlowLevelsSmall : kFlowLevelsLarge;
+}
+
+// Launch schedule: sweeps per launch, at most `levels` each, an EVEN number
 // of launches when iters >= 2 so the ping-pong ends in the caller's buffer.
-std::vector<int> schedule(int iters) {
+std::vector<int> schedule(int iters, int levels) {
     std::vector<int> ks;
     int left = iters;
     while (left > 0) {
-        const int k = std::min(left, kFlowLevels);
+        const int k = std::min(left, levels);
         ks.push_back(k);
         left -= k;
     }
@@ -205,11 +210,14 @@ CF_API int cf_last_cuda_error(void) { return g_last_cuda; }
 
 CF_API int32_t cf_wmc_max_sweeps_per_launch(void) { return kMaxLevels; }
 
-CF_API int32_t cf_wmc_filter_sweeps_per_launch(void) { return kFlowLevels; }
+CF_API int32_t cf_wmc_filter_sweeps_per_launch(int32_t w, int32_t h, int32_t planes) {
+    if (w <= 0 || h <= 0 || planes <= 0) return 0;
+    return flow_levels(w, h, planes);
+}
 
-CF_API int32_t cf_wmc_filter_launches(int32_t iters) {
-    if (iters <= 0) return 0;
-    return (int32_t)schedule(iters).size();
+CF_API int32_t cf_wmc_filter_launches(int32_t w, int32_t h, int32_t planes, int32_t iters) {
+    if (iters <= 0 || w <= 0 || h <= 0 || planes <= 0) return 0;
+    return (int32_t)schedule(iters, flow_levels(w, h, planes)).size();
 }
 
 CF_API void cf_kernel_bank_x12(int32_t* out72) {
@@ -268,7 +276,7 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
     float* ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kWsHeader);
     CF_CUDA(cudaMemsetAsync(flag, 0x7f, sizeof(int32_t), s));
 
-    const std::vector<int> ks = schedule(iters);
+    const std::vector<int> ks = schedule(iters, flow_levels(w, h, planes));
     // Ping-pong between the caller's buffer and the workspace, arranged so
     // the last launch writes `out` (even launch count; iters == 1 copies).
     float* cur = out;

@@ -51,13 +51,13 @@ namespace cfk {
 constexpr int kFastUnroll = CF_FAST_UNROLL;
 // Resident 128-thread blocks per SM the register budget targets (measured on
 // B200, 16384^2): K = 1, 3 and the map run best at 4 blocks
-// (128 registers, K = 3 with a small spill); K = 2, 4 at 3 blocks (168
-// registers, no spills; 4 blocks would spill and lose 16 %).
+// registers); K = 2 at 3 blocks (147 registers with its row-sum carries; 4
+// blocks lose 16-20 % even without spills).
 #ifndef CF_MINB
 #define CF_MINB 4
 #endif
 #ifndef CF_MINB_EVEN
-#define CF_MINB_EVEN 3
+#define CF_MINB_EVEN 3  // K = 2
 #endif
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = 32 * kWarpsPerBlock;
@@ -332,7 +332,11 @@ struct SweepWarp {
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
     f2 acc[K + 1][C];             // non-finite accumulators per level and column
-    f2 hc[K + 1][C], tm[K + 1][C];  // carried row sums per level and pixel pair
+    // Row sums l+r and (a+c)+(l+r) carried down a level from the row above
+    // (K <= 2), or recomputed (K >= 3: the 16 registers buy occupancy there;
+    // measured).  Bit-identical either way.
+    static constexpr bool kCarry = K <= 2;
+    f2 hc[K + 1][C], tm[K + 1][C];
     f2 onv[K + 1][C];               // results of the current step, per level
     // kModeL1: the dual d_L(y) a level produces is consumed pointwise by
     // level L+1 two steps later (same lane, same columns): a 2-deep register
@@ -441,7 +445,7 @@ struct SweepWarp {
         lds_nb(am + (lbase - sbase), m);
         lds_nb(ao + (lbase - sbase), o);
         lds_nb(ap + (lbase - sbase), p);
-        if (CHECKED && y == rlo(L)) {  // first row of this level: no carries yet
+        if (kCarry && CHECKED && y == rlo(L)) {  // first row of this level: no carries yet
 #pragma unroll
             for (int j = 1; j <= C; ++j) {
                 hc[L][j - 1] = add2(o[j - 1], o[j + 1]);                        // l+r
@@ -458,11 +462,17 @@ struct SweepWarp {
         for (int j = 1; j <= C; ++j) {
             PairD D;
             f2 hb, t0;
-            pair_d(m[j - 1], m[j], m[j + 1], o[j - 1], o[j], o[j + 1], p[j - 1], p[j], p[j + 1],
-                   W[j - 1], W[j],
-                   hc[L][j - 1], tm[L][j - 1], hb, t0, D);
-            hc[L][j - 1] = hb;
-            tm[L][j - 1] = t0;
+            if constexpr (kCarry) {
+                pair_d(m[j - 1], m[j], m[j + 1], o[j - 1], o[j], o[j + 1], p[j - 1], p[j],
+                       p[j + 1], W[j - 1], W[j], hc[L][j - 1], tm[L][j - 1], hb, t0, D);
+                hc[L][j - 1] = hb;
+                tm[L][j - 1] = t0;
+            } else {  // recompute the row sums (bit-identical to the carried ones)
+                const f2 hcr = add2(o[j - 1], o[j + 1]);
+                const f2 tmr = add2(add2(m[j - 1], m[j + 1]), hcr);
+                pair_d(m[j - 1], m[j], m[j + 1], o[j - 1], o[j], o[j + 1], p[j - 1], p[j],
+                       p[j + 1], W[j - 1], W[j], hcr, tmr, hb, t0, D);
+            }
             const f2 b = select_pair(D);
             f2 hw = mul2(b, kC12x2);
             if constexpr (MAP) {
@@ -684,7 +694,7 @@ template <int K, int MODE>
 // The solver modes carry f (and the dual FIFO): 3 blocks/SM = 168 registers,
 // no spills at K = 3.
 __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
-                                           : (MODE == kModeFlow && K % 2 == 0) ? CF_MINB_EVEN
+                                           : (MODE == kModeFlow && K == 2)     ? CF_MINB_EVEN
                                                                                : CF_MINB)
     wmc_sweeps_kernel(const SweepParams p) {
     constexpr bool MAP = MODE == kModeMap;

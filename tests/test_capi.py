@@ -65,13 +65,20 @@ def test_invalid_arguments_rejected_before_cuda():
                                     None) == EINVAL                               # src too short
 
 
-def test_filter_schedule_is_even():
+@pytest.mark.parametrize("w,h,planes,levels", [(1024, 1024, 1, 2), (2048, 2048, 1, 2),
+                                               (2049, 2048, 1, 3), (16384, 16384, 1, 3),
+                                               (1920, 1080, 256, 3), (3840, 2160, 3, 3)])
+def test_filter_schedule_is_even(w, h, planes, levels):
+    """Sweeps per launch by working-set size; an even launch
+    count for iters >= 2 so the ping-pong ends in the caller's buffer."""
     L = cf.lib()
-    assert L.cf_wmc_filter_launches(0) == 0
-    assert L.cf_wmc_filter_launches(1) == 1
+    assert L.cf_wmc_filter_sweeps_per_launch(w, h, planes) == levels
+    assert L.cf_wmc_filter_sweeps_per_launch(0, h, planes) == 0
+    assert L.cf_wmc_filter_launches(w, h, planes, 0) == 0
+    assert L.cf_wmc_filter_launches(w, h, planes, 1) == 1
     for it in (2, 3, 5, 20, 50, 99, 100, 200):
-        n = L.cf_wmc_filter_launches(it)
-        assert n % 2 == 0 and n >= it / L.cf_wmc_max_sweeps_per_launch()
+        n = L.cf_wmc_filter_launches(w, h, planes, it)
+        assert n % 2 == 0 and n >= it / levels and n <= it
 
 
 def test_generator_deterministic_and_in_range():
