@@ -153,24 +153,17 @@ int flow_levels(int32_t w, int32_t h, int32_t planes) {
 }
 
 // Launch schedule: sweeps per launch, at most `levels` each, an EVEN number
-// of launches when iters >= 2 so the ping-pong ends in the caller's buffer.
+// of launches when iters >= 2 so the ping-pong ends in the caller's buffer:
+// n = the smallest even count >= ceil(iters / levels), sweeps spread evenly
+// (200 at 3 levels -> 64 x 3 + 4 x 2: no single-sweep launch, each of which
+// would cost a full HBM pass).
 std::vector<int> schedule(int iters, int levels) {
-    std::vector<int> ks;
-    int left = iters;
-    while (left > 0) {
-        const int k = std::min(left, levels);
-        ks.push_back(k);
-        left -= k;
-    }
-    if (ks.size() % 2 == 1 && iters >= 2) {
-        // split the largest launch (>= 2 sweeps) into two
-        auto it = std::max_element(ks.begin(), ks.end());
-        const int k = *it;
-        if (k >= 2) {
-            *it = k / 2;
-            ks.insert(it + 1, k - k / 2);
-        }
-    }
+    if (iters <= 0) return {};
+    if (iters == 1) return {1};
+    int n = (iters + levels - 1) / levels;
+    n += n & 1;
+    std::vector<int> ks(n, iters / n);
+    for (int i = 0; i < iters % n; ++i) ks[i] += 1;
     return ks;
 }
 

@@ -69,7 +69,10 @@ constexpr int C = CF_COLS;            // columns per lane per chunk (2 or 4)
 static_assert(C == 2 || C == 4, "2 or 4 columns per lane");
 constexpr int kChunk = 32 * C;        // columns per chunk window
 constexpr int kRowBytes = 8 * (kChunk + 2);   // pairs for columns -1 .. kChunk
-constexpr int kRD = 5;                // level-0 prefetch distance (rows)
+#ifndef CF_RD
+#define CF_RD 5
+#endif
+constexpr int kRD = CF_RD;            // level-0 prefetch distance (rows); kRD + 3 a power of 2
 constexpr int kRS = kRD + 3;          // level-0 ring slots (rows t-2 .. t+RD)
 static_assert((kRS & (kRS - 1)) == 0, "ring slots must be a power of two");
 
