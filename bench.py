@@ -197,7 +197,9 @@ def bench_b200(args, cfg):
     if world > 1 and cfg.sharding == "images":
         host = host[p0:p1]
     host_t = torch.from_numpy(np.ascontiguousarray(host)).pin_memory()
-    out_host = torch.empty(host_t.shape, dtype=torch.float32).pin_memory()
+    # u8 frames in -> u8 frames out (save-time rounding); f32 otherwise
+    out_dtype = torch.uint8 if cfg.u8 else torch.float32
+    out_host = torch.empty(host_t.shape, dtype=out_dtype).pin_memory()
     dev_in = host_t.to(dev)
     n_px_local = int(np.prod(host.shape))
     P, H, W = (host.shape if host.ndim == 3 else (1,) + host.shape)
@@ -233,10 +235,16 @@ def bench_b200(args, cfg):
         # first_bad_iter = NULL: no host sync inside the step (capturable);
         # the device flag is checked once after the timed region.
         if cfg.u8:
+            out8 = torch.empty(dev_in.shape, dtype=torch.uint8, device=dev)
+            nb8 = int(L.cf_wmc_filter_u8_u8_workspace_bytes(W, H, P))
+            ws8 = torch.empty(nb8, dtype=torch.uint8, device=dev)
+            f32_bytes = (P * H * W * 4 + 255) // 256 * 256  # the filter workspace follows
+            flag_ws = ws8[f32_bytes:]
+
             def step():
-                rc = L.cf_wmc_filter_u8_f32(dev_in.data_ptr(), W, H * W, work.data_ptr(), W, H,
-                                            W, P, H * W, cfg.iters, cfg.dt, ws.data_ptr(),
-                                            nbytes, None, cur_sp())
+                rc = L.cf_wmc_filter_u8_u8(dev_in.data_ptr(), W, H * W, out8.data_ptr(), W,
+                                           H * W, W, H, P, cfg.iters, cfg.dt, ws8.data_ptr(),
+                                           nb8, None, cur_sp())
                 assert rc == 0, rc
         else:
             def step():
@@ -244,7 +252,8 @@ def bench_b200(args, cfg):
                 rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, cfg.iters, cfg.dt,
                                          ws.data_ptr(), nbytes, None, cur_sp())
                 assert rc == 0, rc
-        launches_per_step = int(L.cf_wmc_filter_launches(W, H, P, cfg.iters))
+        launches_per_step = int(L.cf_wmc_filter_launches(W, H, P, cfg.iters)) + (2 if cfg.u8
+                                                                                 else 0)
 
     def barrier():
         if world > 1:
@@ -293,7 +302,8 @@ def bench_b200(args, cfg):
     if ws is not None:  # device non-finite flag of the last timed step
         import ctypes
         bad = ctypes.c_int32(0)
-        rc = L.cf_wmc_filter_query_nonfinite(ws.data_ptr(), ctypes.byref(bad), sp)
+        rc = L.cf_wmc_filter_query_nonfinite((flag_ws if cfg.u8 else ws).data_ptr(),
+                                             ctypes.byref(bad), sp)
         assert rc == 0, f"non-finite value in the timed run (iteration {bad.value})"
     updates_job = cfg.updates  # whole job over all ranks (strong scaling for rows)
     if world > 1 and cfg.sharding == "images":
@@ -314,7 +324,9 @@ def bench_b200(args, cfg):
             rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, 2 * K, cfg.dt,
                                      ws.data_ptr(), nbytes, None, sp)
             assert rc == 0, rc
-        if not cfg.u8:  # u8: `work` already holds the widened fp32 result of the steps
+        if cfg.u8:  # measurement input: the widened frames (q/255)
+            work.copy_(dev_in.to(torch.float32).div_(255.0))
+        else:
             work.copy_(dev_in)
         for _ in range(2):
             two_launches()
@@ -341,9 +353,11 @@ def bench_b200(args, cfg):
     if pipelined:
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         dbufs = [torch.empty(host_t.shape, dtype=host_t.dtype, device=dev) for _ in range(2)]
-        obufs = [torch.empty(out_host.shape, dtype=torch.float32, device=dev) for _ in range(2)]
-        wss = [torch.empty(int(L.cf_wmc_filter_workspace_bytes(W, H, W, P, H * W)),
-                           dtype=torch.uint8, device=dev) for _ in range(2)]
+        obufs = [torch.empty(out_host.shape, dtype=out_dtype, device=dev) for _ in range(2)]
+        ws_e2e = int(L.cf_wmc_filter_u8_u8_workspace_bytes(W, H, P) if cfg.u8 else
+                     L.cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+        flag_off = (P * H * W * 4 + 255) // 256 * 256 if cfg.u8 else 0
+        wss = [torch.empty(ws_e2e, dtype=torch.uint8, device=dev) for _ in range(2)]
         ev_out = [torch.cuda.Event() for _ in range(2)]
         for e in ev_out:
             e.record(s_out)
@@ -365,12 +379,14 @@ def bench_b200(args, cfg):
                 res = obufs[b]
             elif cfg.u8:
                 res = cf.mc_flow_u8(dbufs[b], cf.FlowConfig(dt=cfg.dt, iters=cfg.iters),
-                                    workspace=wss[b], out=obufs[b], check_finite=False)
+                                    workspace=wss[b], out=obufs[b], check_finite=False,
+                                    out_dtype="u8")
             else:
                 res = cf.mc_flow(dbufs[b], cf.FlowConfig(dt=cfg.dt, iters=cfg.iters),
                                  workspace=wss[b], inplace=True, check_finite=False)
             if cfg.iters > 0:  # non-finite flag of this step (device check), read async
-                flag_host[b:b + 1].copy_(wss[b][:4].view(torch.int32), non_blocking=True)
+                flag_host[b:b + 1].copy_(wss[b][flag_off:flag_off + 4].view(torch.int32),
+                                         non_blocking=True)
             ev_c = torch.cuda.Event()
             ev_c.record(stream)
             with torch.cuda.stream(s_out):

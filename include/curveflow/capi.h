@@ -170,6 +170,15 @@ CF_API int cf_image8_to_planes_f32(const uint8_t* in, int64_t in_pitch, int32_t 
 CF_API int cf_planes_f32_to_image8(const float* planes, int64_t pitch, int64_t plane_stride,
                                    int32_t w, int32_t h, int32_t channels, uint8_t* out,
                                    int64_t out_pitch, void* stream);
+/* mc_flow on a planar batch of 8-bit images (planes independent): widen    */
+/* q/255, filter, re-quantise rint(clamp(v,0,1)*255) -- u8 frames in, u8     */
+/* frames out.  Workspace: cf_wmc_filter_u8_u8_workspace_bytes.*/
+CF_API size_t cf_wmc_filter_u8_u8_workspace_bytes(int32_t w, int32_t h, int32_t planes);
+CF_API int cf_wmc_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
+                               uint8_t* out, int64_t out_pitch, int64_t out_plane_stride,
+                               int32_t w, int32_t h, int32_t planes, int32_t iters, float dt,
+                               void* workspace, size_t workspace_bytes, int32_t* first_bad_iter,
+                               void* stream);
 /* mc_flow on an interleaved 8-bit image, per channel, result re-quantised. */
 CF_API size_t cf_wmc_filter_image8_workspace_bytes(int32_t w, int32_t h, int32_t channels);
 CF_API int cf_wmc_filter_image8(const uint8_t* in, int64_t in_pitch, uint8_t* out,

@@ -168,14 +168,15 @@ std::vector<int> schedule(int iters, int levels) {
 }
 
 __global__ void u8_to_f32_kernel(const uint8_t* in, int64_t in_pitch, int64_t in_plane, float* out,
-                                 int64_t pitch, int64_t plane, int32_t w, int32_t h) {
-    const int64_t n = (int64_t)w * h;
-    const int p = blockIdx.y;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = i / w, x = i % w;
-        out[p * plane + y * pitch + x] =
-            __fdiv_rn((float)in[p * in_plane + y * in_pitch + x], 255.0f);
+                                 int64_t pitch, int64_t plane, int32_t w, int32_t h,
+                                 int32_t planes) {
+    // one row per block iteration: a single index division per row
+    const int64_t rows = (int64_t)h * planes;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t p = r / h, y = r - p * h;
+        const uint8_t* src = in + p * in_plane + y * in_pitch;
+        float* dst = out + p * plane + y * pitch;
+        for (int x = threadIdx.x; x < w; x += blockDim.x) dst[x] = __fdiv_rn((float)src[x], 255.0f);
     }
 }
 
@@ -280,9 +281,8 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
         // widen u8 -> fp32 into whichever buffer makes the
         // final launch land in `out`
         if (ks.size() % 2 == 1) std::swap(cur, nxt);
-        dim3 grid(1184, planes);
-        u8_to_f32_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(src0), src_pitch,
-                                               src_plane, cur, pitch, plane_stride, w, h);
+        u8_to_f32_kernel<<<148 * 16, 256, 0, s>>>(static_cast<const uint8_t*>(src0), src_pitch,
+                                               src_plane, cur, pitch, plane_stride, w, h, planes);
         CF_CUDA(cudaGetLastError());
     }
     int iter = 0;
@@ -345,9 +345,8 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
     if (first_bad_iter) *first_bad_iter = 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (iters == 0) {
-        dim3 grid(1184, planes);
-        u8_to_f32_kernel<<<grid, 256, 0, s>>>(in, in_pitch, in_plane_stride, out, pitch,
-                                               plane_stride, w, h);
+        u8_to_f32_kernel<<<148 * 16, 256, 0, s>>>(in, in_pitch, in_plane_stride, out, pitch,
+                                               plane_stride, w, h, planes);
         CF_CUDA(cudaGetLastError());
         return CF_OK;
     }

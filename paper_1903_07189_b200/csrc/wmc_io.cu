@@ -1,5 +1,6 @@
-// paper_1903_07189_b200/csrc/wmc_io.cu -- the 8-bit interleaved image format
-// on either side of the WMC filter.
+// paper_1903_07189_b200/csrc/wmc_io.cu -- 8-bit images on either side of the
+// WMC filter: interleaved 1/3-channel images and
+// planar u8 batches (cfg5 frames in, frames out).
 //
 // Reference semantics: images are processed per channel (SPEC.md:62-69,
 // PAPER.md:674 "performed on each color channel separately"); 8-bit inputs
@@ -23,13 +24,11 @@ constexpr size_t align256(size_t n) { return (n + 255) & ~(size_t)255; }
 __global__ void deinterleave_kernel(const uint8_t* __restrict__ in, int64_t in_pitch, int32_t w,
                                     int32_t h, int32_t ch, float* __restrict__ out,
                                     int64_t pitch, int64_t plane_stride) {
-    const int64_t n = (int64_t)w * h;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = i / w, x = i % w;
-        const uint8_t* px = in + y * in_pitch + x * ch;
-        for (int c = 0; c < ch; ++c)
-            out[c * plane_stride + y * pitch + x] = __fdiv_rn((float)px[c], 255.0f);
+    for (int64_t y = blockIdx.x; y < h; y += gridDim.x) {
+        const uint8_t* row = in + y * in_pitch;
+        for (int x = threadIdx.x; x < w; x += blockDim.x)
+            for (int c = 0; c < ch; ++c)
+                out[c * plane_stride + y * pitch + x] = __fdiv_rn((float)row[x * ch + c], 255.0f);
     }
 }
 
@@ -41,12 +40,25 @@ __device__ __forceinline__ uint8_t quantize(float v) {
 __global__ void interleave_kernel(const float* __restrict__ in, int64_t pitch,
                                   int64_t plane_stride, int32_t w, int32_t h, int32_t ch,
                                   uint8_t* __restrict__ out, int64_t out_pitch) {
-    const int64_t n = (int64_t)w * h;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = i / w, x = i % w;
-        uint8_t* px = out + y * out_pitch + x * ch;
-        for (int c = 0; c < ch; ++c) px[c] = quantize(in[c * plane_stride + y * pitch + x]);
+    for (int64_t y = blockIdx.x; y < h; y += gridDim.x) {
+        uint8_t* row = out + y * out_pitch;
+        for (int x = threadIdx.x; x < w; x += blockDim.x)
+            for (int c = 0; c < ch; ++c) row[x * ch + c] = quantize(in[c * plane_stride + y * pitch + x]);
+    }
+}
+
+// Planar quantisation of a batch (one byte per pixel per plane).
+__global__ void quantize_planes_kernel(const float* __restrict__ in, int64_t pitch,
+                                       int64_t plane_stride, int32_t w, int32_t h, int32_t planes,
+                                       uint8_t* __restrict__ out, int64_t out_pitch,
+                                       int64_t out_plane_stride) {
+    // one row per block iteration: a single index division per row
+    const int64_t rows = (int64_t)h * planes;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t p = r / h, y = r - p * h;
+        const float* src = in + p * plane_stride + y * pitch;
+        uint8_t* dst = out + p * out_plane_stride + y * out_pitch;
+        for (int x = threadIdx.x; x < w; x += blockDim.x) dst[x] = quantize(src[x]);
     }
 }
 
@@ -76,7 +88,7 @@ CF_API int cf_image8_to_planes_f32(const uint8_t* in, int64_t in_pitch, int32_t 
                                    int64_t plane_stride, void* stream) {
     if (!in || !planes || !io_shape_ok(w, h, channels, in_pitch, pitch, plane_stride))
         return CF_EINVAL;
-    deinterleave_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(in, in_pitch, w, h, channels,
+    deinterleave_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(in, in_pitch, w, h, channels,
                                                                  planes, pitch, plane_stride);
     return io_launch_check();
 }
@@ -86,7 +98,7 @@ CF_API int cf_planes_f32_to_image8(const float* planes, int64_t pitch, int64_t p
                                    int64_t out_pitch, void* stream) {
     if (!planes || !out || !io_shape_ok(w, h, channels, out_pitch, pitch, plane_stride))
         return CF_EINVAL;
-    interleave_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(planes, pitch, plane_stride, w, h,
+    interleave_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(planes, pitch, plane_stride, w, h,
                                                                channels, out, out_pitch);
     return io_launch_check();
 }
@@ -119,6 +131,37 @@ CF_API int cf_wmc_filter_image8(const uint8_t* in, int64_t in_pitch, uint8_t* ou
                            first_bad_iter, stream);
     if (rc) return rc;
     return cf_planes_f32_to_image8(planes, w, plane, w, h, channels, out, out_pitch, stream);
+}
+
+CF_API size_t cf_wmc_filter_u8_u8_workspace_bytes(int32_t w, int32_t h, int32_t planes) {
+    if (w <= 0 || h <= 0 || planes <= 0) return 0;
+    const int64_t plane = (int64_t)w * h;
+    return align256((size_t)(planes * plane) * sizeof(float)) +
+           cf_wmc_filter_workspace_bytes(w, h, w, planes, plane);
+}
+
+CF_API int cf_wmc_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
+                               uint8_t* out, int64_t out_pitch, int64_t out_plane_stride,
+                               int32_t w, int32_t h, int32_t planes, int32_t iters, float dt,
+                               void* workspace, size_t workspace_bytes, int32_t* first_bad_iter,
+                               void* stream) {
+    if (!in || !out || !workspace || w <= 0 || h <= 0 || planes <= 0 || iters < 0)
+        return CF_EINVAL;
+    if (in_pitch < w || out_pitch < w) return CF_EINVAL;
+    if (planes > 1 && (in_plane_stride < in_pitch * (int64_t)h ||
+                       out_plane_stride < out_pitch * (int64_t)h))
+        return CF_EINVAL;
+    if (workspace_bytes < cf_wmc_filter_u8_u8_workspace_bytes(w, h, planes)) return CF_EINVAL;
+    const int64_t plane = (int64_t)w * h;
+    float* f = reinterpret_cast<float*>(workspace);
+    const size_t off = align256((size_t)(planes * plane) * sizeof(float));
+    int rc = cf_wmc_filter_u8_f32(in, in_pitch, in_plane_stride, f, w, h, w, planes, plane, iters,
+                                  dt, reinterpret_cast<char*>(workspace) + off,
+                                  workspace_bytes - off, first_bad_iter, stream);
+    if (rc) return rc;
+    quantize_planes_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(
+        f, w, plane, w, h, planes, out, out_pitch, out_plane_stride);
+    return io_launch_check();
 }
 
 }  // extern "C"

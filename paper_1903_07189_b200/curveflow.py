@@ -162,11 +162,16 @@ def mc_flow(img, cfg: FlowConfig, *, check_finite: bool = True, workspace=None,
     return res
 
 
-def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=None, out=None):
+def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=None, out=None,
+               out_dtype: str = "f32"):
     """8-bit input widened on device as q/255 (BASELINE cfg 5), then
-    mc_flow; returns float32 U^iters of the same (P, H, W) / (H, W) shape."""
+    mc_flow; returns float32 U^iters of the same (P, H, W) / (H, W) shape, or,
+    with out_dtype="u8", the frames re-quantised on device
+    (rint(clamp(U, 0, 1) * 255), the reference's save-time rounding)."""
     torch = _torch()
     cfg.validate()
+    if out_dtype not in ("f32", "u8"):
+        raise ValueError("out_dtype must be 'f32' or 'u8'")
     if isinstance(img_u8, np.ndarray):
         src = torch.from_numpy(np.ascontiguousarray(img_u8, dtype=np.uint8)).cuda()
         host = True
@@ -178,6 +183,25 @@ def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=
         raise TypeError("mc_flow_u8 expects uint8 input")
     s3, squeeze = _as_planes(src)
     P, H, W = s3.shape
+    if out_dtype == "u8":
+        if out is None:
+            out = torch.empty((P, H, W), dtype=torch.uint8, device=s3.device)
+        nbytes = int(lib().cf_wmc_filter_u8_u8_workspace_bytes(W, H, P))
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = torch.empty(nbytes, dtype=torch.uint8, device=s3.device)
+        bad = C.c_int32(0)
+        with torch.cuda.device(s3.device):
+            rc = lib().cf_wmc_filter_u8_u8(
+                s3.data_ptr(), W, H * W, out.data_ptr(), W, H * W, W, H, P, int(cfg.iters),
+                float(cfg.dt), workspace.data_ptr(), nbytes,
+                C.byref(bad) if check_finite else None, _stream_ptr(torch, s3.device))
+        if rc == CF_ENONFINITE:
+            raise FlowError(bad.value)
+        check(rc, "mc_flow_u8")
+        res = out[0] if squeeze else out
+        if host:
+            return res.cpu().numpy() if isinstance(img_u8, np.ndarray) else res.cpu()
+        return res
     if out is None:
         out = torch.empty((P, H, W), dtype=torch.float32, device=s3.device)
     nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))

@@ -282,6 +282,27 @@ def test_data_fidelity_bitexact():
     assert cf.data_fidelity(u, None, 2.0) == oracle.fidelity(u, None, 2.0)
 
 
+@pytest.mark.parametrize("planes,h,w,iters", [(1, 37, 150, 0), (3, 64, 129, 1), (5, 45, 77, 6),
+                                               (2, 130, 257, 20)])
+def test_filter_u8_to_u8_bitexact(planes, h, w, iters):
+    """Planar u8 batch in, u8 out (cfg5 frames): widen q/255, filter,
+    rint(clamp(U,0,1)*255) -- bit-exact vs the oracle's three steps."""
+    rng = np.random.default_rng(planes * 100 + iters)
+    img = np.stack([cf.synth_image(h, w, seed=int(rng.integers(1 << 30)), n_rects=5, n_discs=5,
+                                   sigma=0.1) for _ in range(planes)])
+    q = np.rint(img * 255).astype(np.uint8)
+    got = cf.mc_flow_u8(torch.from_numpy(q).cuda(), cf.FlowConfig(iters=iters),
+                        out_dtype="u8").cpu().numpy()
+    ref_f, bad = oracle.flow_f32(oracle.u8_to_f32(q), iters, 1.0) if iters else \
+        (oracle.u8_to_f32(q), 0)
+    assert bad == 0
+    assert got.dtype == np.uint8 and got.shape == q.shape
+    assert np.array_equal(got, oracle.quantize_u8(ref_f))
+    # the fp32 output of the same call path equals the un-quantised oracle
+    f32 = cf.mc_flow_u8(q, cf.FlowConfig(iters=iters))
+    assert_bitexact(f32, ref_f, "u8->f32")
+
+
 @pytest.mark.parametrize("q", [1.0, 2.0, 0.5])
 def test_wmc_energy_bitexact(q):
     img = np.stack([cf.synth_image(67, 201, seed=70 + s, n_rects=5, n_discs=5, sigma=0.1)
