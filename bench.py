@@ -118,13 +118,16 @@ def dist_env():
     return world, rank, local
 
 
-def make_input(cfg, rows=None, threads=0):
-    """Seeded synthetic input (host numpy), all planes; rows = (r0, r1) crop."""
+def make_input(cfg, rows=None, threads=0, planes=None):
+    """Seeded synthetic input (host numpy); rows = (r0, r1) crop, planes =
+    (p0, p1) subset (plane p keeps its own seed, so shards equal the slices
+    of the full batch)."""
     import numpy as np
 
     import paper_1903_07189_b200 as cf
     imgs = []
-    for p in range(cfg.planes):
+    p0, p1 = planes if planes is not None else (0, cfg.planes)
+    for p in range(p0, p1):
         a = cf.synth_image(cfg.h, cfg.w, cfg.seed(p), cfg.n_rects, cfg.n_discs, cfg.sigma,
                            dtype="u8" if cfg.u8 else "f32", threads=threads)
         imgs.append(a if rows is None else a[rows[0]:rows[1]])
@@ -193,9 +196,10 @@ def bench_b200(args, cfg):
         rows = None
     else:
         rows = None
-    host = make_input(cfg, rows=rows)
-    if world > 1 and cfg.sharding == "images":
-        host = host[p0:p1]
+    # each rank generates only its share, on its share of the host cores
+    gen_threads = 0 if world == 1 else max(1, (os.cpu_count() or 1) // world)
+    host = make_input(cfg, rows=rows, threads=gen_threads,
+                      planes=(p0, p1) if world > 1 and cfg.sharding == "images" else None)
     host_t = torch.from_numpy(np.ascontiguousarray(host)).pin_memory()
     # u8 frames in -> u8 frames out (save-time rounding); f32 otherwise
     out_dtype = torch.uint8 if cfg.u8 else torch.float32
