@@ -225,7 +225,8 @@ def bench_b200(args, cfg):
         buf_a = torch.zeros((lay.rows, cfg.w), dtype=torch.float32, device=dev)
         buf_b = torch.zeros_like(buf_a)
         flag = torch.full((1,), 0x7F7F7F7F, dtype=torch.int32, device=dev)
-        flow = sharded.ShardedFlow(lay, sharded.cuda_compute(flag), dist)
+        flow = sharded.ShardedFlow(lay, sharded.cuda_compute(flag), dist,
+                                   side_stream=torch.cuda.Stream(dev))
 
         def step():
             buf_a[lay.band_slice()].copy_(dev_in)

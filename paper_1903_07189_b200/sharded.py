@@ -3,11 +3,12 @@
 One process per GPU.  The image's rows are split like the reference's
 ``curveflow::parallel::for_rows`` (contiguous ceil-div blocks,
 proj/include/curveflow/parallel.hpp:36-44); each rank owns one band and keeps
-``k`` halo rows above and below it.  Before every launch of ``kk <= k`` fused
-sweeps the ranks exchange the ``kk`` boundary rows of the current iterate with
-their neighbours (point-to-point over NCCL / NVLink; gloo in the CPU tests),
-then each rank advances its band ``kk`` iterations with the row-band kernel
-(C-ABI ``cf_wmc_sweeps_band_f32``).  Jacobi semantics make the result
+``k`` halo rows above and below it.  Each launch of ``kk <= k`` fused sweeps
+needs the ``kk`` boundary rows of the current iterate from the neighbours
+(point-to-point over NCCL / NVLink; gloo in the CPU tests); each rank
+advances its band with the row-band kernel (C-ABI
+``cf_wmc_sweeps_band_f32``), computing the rows its neighbours need first so
+the exchange overlaps the band interior (ShardedFlow, overlap=True).  Jacobi semantics make the result
 bit-identical to the single-GPU filter for any band count.
 
 The compute step is injected, so the exchange protocol is the same code in
@@ -68,16 +69,27 @@ class BandLayout:
 
 
 class ShardedFlow:
-    """Sharded mc_flow over a band buffer pair (torch tensors, any device)."""
+    """Sharded mc_flow over a band buffer pair (torch tensors, any device).
 
-    def __init__(self, layout: BandLayout, compute: ComputeFn, dist, group=None):
+    overlap=True (default): each launch first computes the rows the
+    neighbours will need for the NEXT launch (the band's top / bottom kk'
+    rows), starts the halo exchange of those rows, and computes the band
+    interior meanwhile -- on `side_stream` when given (CUDA), so the
+    point-to-point transfer hides behind the interior sweep.  The rows each
+    call produces are disjoint and all read the same iterate, so the result is
+    bit-identical to overlap=False (exchange, then one band launch).
+    """
+
+    def __init__(self, layout: BandLayout, compute: ComputeFn, dist, group=None,
+                 overlap: bool = True, side_stream=None):
         self.L = layout
         self.compute = compute
         self.dist = dist
         self.group = group
+        self.overlap = overlap
+        self.side = side_stream
 
-    def exchange(self, buf, kk: int) -> None:
-        """Fill the kk halo rows nearest the band from the neighbours' bands."""
+    def _ops(self, buf, kk: int):
         L, dist = self.L, self.dist
         ops = []
         b0, b1 = L.top, L.top + (L.r1 - L.r0)
@@ -87,22 +99,76 @@ class ShardedFlow:
         if L.rank < L.world - 1:
             ops.append(dist.P2POp(dist.isend, buf[b1 - kk:b1], L.rank + 1, self.group))
             ops.append(dist.P2POp(dist.irecv, buf[b1:b1 + kk], L.rank + 1, self.group))
+        return ops
+
+    def exchange(self, buf, kk: int) -> None:
+        """Fill the kk halo rows nearest the band from the neighbours' bands."""
+        ops = self._ops(buf, kk)
         if ops:
-            for req in dist.batch_isend_irecv(ops):
+            for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+
+    def _band(self, cur, nxt, y0: int, y1: int, kk: int, dt: float, it: int) -> None:
+        if y1 > y0:
+            L = self.L
+            self.compute(cur, L.buf_row0, nxt, L.buf_row0, L.h, y0, y1, kk, dt, it)
 
     def run(self, buf_a, buf_b, iters: int, dt: float):
         """buf_a holds U^0 in its band rows; returns the buffer holding U^iters."""
         L = self.L
         cur, nxt = buf_a, buf_b
+        sched = launch_schedule(iters, L.k)
+        if not sched:
+            return cur
+        self.exchange(cur, sched[0])
         it = 0
-        for kk in launch_schedule(iters, L.k):
-            self.exchange(cur, kk)
+        for i, kk in enumerate(sched):
+            nk = sched[i + 1] if i + 1 < len(sched) else 0
             # src covers [max(0, r0-kk), min(h, r1+kk)); dst rows [r0, r1)
-            self.compute(cur, L.buf_row0, nxt, L.buf_row0, L.h, L.r0, L.r1, kk, dt, it)
+            if not self.overlap or nk == 0 or L.world == 1:
+                self._band(cur, nxt, L.r0, L.r1, kk, dt, it)
+                if nk:
+                    self.exchange(nxt, nk)
+            else:
+                top = nk if L.rank > 0 else 0
+                bot = nk if L.rank < L.world - 1 else 0
+                # rows the neighbours need next (clipped to the band)
+                t1 = min(L.r0 + top, L.r1)
+                b0 = max(L.r1 - bot, t1)
+                ready = self._mark()              # cur (with its halo) is final here
+                self._band(cur, nxt, L.r0, t1, kk, dt, it)
+                self._band(cur, nxt, b0, L.r1, kk, dt, it)
+                reqs = self.dist.batch_isend_irecv(self._ops(nxt, nk))
+                self._interior(cur, nxt, t1, b0, kk, dt, it, ready)
+                for req in reqs:
+                    req.wait()
+                self._join()
             it += kk
             cur, nxt = nxt, cur
         return cur
+
+    def _mark(self):
+        if self.side is None:
+            return None
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.side.device))
+        return ev
+
+    def _interior(self, cur, nxt, y0: int, y1: int, kk: int, dt: float, it: int,
+                  ready=None) -> None:
+        if self.side is None:
+            self._band(cur, nxt, y0, y1, kk, dt, it)
+            return
+        import torch
+        self.side.wait_event(ready)   # not the boundary kernels: their rows are disjoint
+        with torch.cuda.stream(self.side):
+            self._band(cur, nxt, y0, y1, kk, dt, it)
+
+    def _join(self) -> None:
+        if self.side is not None:
+            import torch
+            torch.cuda.current_stream(self.side.device).wait_stream(self.side)
 
 
 def cuda_compute(flag=None) -> ComputeFn:

@@ -343,3 +343,73 @@ def test_extreme_aspect_ratios(h, w):
     got = cf.mc_flow(d, cf.FlowConfig(iters=5)).cpu().numpy()
     ref, _ = oracle.flow_f32(img, 5, 1.0)
     assert_bitexact(got, ref, f"flow {h}x{w}")
+
+
+class _ThreadDist:
+    """torch.distributed stand-in for ranks simulated as host threads on ONE
+    GPU: a send enqueues a device copy plus an event on the sender's current
+    stream; a receive makes the receiver's current stream wait on that event
+    and copies.  All waiting is host-side (queues) -- no kernel waits on
+    another -- so this checks the overlap schedule's stream/event ordering."""
+
+    isend, irecv = "send", "recv"
+
+    def __init__(self, rank, boxes):
+        self.rank, self.boxes = rank, boxes
+
+    def P2POp(self, op, t, peer, group=None):
+        return (op, t, peer)
+
+    def batch_isend_irecv(self, ops):
+        s = torch.cuda.current_stream()
+        for op, t, peer in ops:
+            if op == "send":
+                c = t.clone()
+                ev = torch.cuda.Event()
+                ev.record(s)
+                self.boxes[(self.rank, peer)].put((c, ev))
+        for op, t, peer in ops:
+            if op == "recv":
+                c, ev = self.boxes[(peer, self.rank)].get(timeout=120)
+                s.wait_event(ev)
+                t.copy_(c)
+        return []
+
+
+@pytest.mark.parametrize("world,iters", [(2, 10), (3, 11)])
+def test_sharded_overlap_streams_on_one_gpu(world, iters):
+    """Row-band flow with the boundary-first / interior-on-a-side-stream
+    schedule (sharded.ShardedFlow, the N > 1 bench path) equals the
+    single-GPU filter bit for bit."""
+    import queue
+    import threading
+    from paper_1903_07189_b200 import sharded
+    h, w = 150, 233
+    img = cf.synth_image(h, w, seed=31, n_rects=6, n_discs=6, sigma=0.1)
+    ref = cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(iters=iters)).cpu().numpy()
+    k = int(cf.lib().cf_wmc_filter_sweeps_per_launch(w, h, 1))
+    boxes = {(a, b): queue.Queue() for a in range(world) for b in range(world)}
+    out, errs = np.empty_like(img), []
+
+    def rank_main(r):
+        try:
+            lay = sharded.BandLayout(h, w, r, world, k)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                a = torch.zeros((lay.rows, w), dtype=torch.float32, device="cuda")
+                b = torch.zeros_like(a)
+                a[lay.band_slice()] = torch.from_numpy(img[lay.r0:lay.r1]).cuda()
+                flow = sharded.ShardedFlow(lay, sharded.cuda_compute(), _ThreadDist(r, boxes),
+                                           side_stream=torch.cuda.Stream())
+                res = flow.run(a, b, iters, 1.0)
+                band = res[lay.band_slice()].cpu().numpy()
+            out[lay.r0:lay.r1] = band
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    assert_bitexact(out, ref, f"sharded world={world}")
