@@ -118,6 +118,12 @@ def dist_env():
     return world, rank, local
 
 
+def workload_name(cfg) -> str:
+    """The config's name in both arms' JSON lines."""
+    return (f"{cfg.name}: {cfg.planes}x{cfg.h}x{cfg.w} {'u8' if cfg.u8 else 'f32'}, "
+            f"{cfg.iters or 1} {'iterations' if cfg.iters else 'map evaluation'}, dt={cfg.dt}")
+
+
 def make_input(cfg, rows=None, threads=0, planes=None):
     """Seeded synthetic input (host numpy); rows = (r0, r1) crop, planes =
     (p0, p1) subset (plane p keeps its own seed, so shards equal the slices
@@ -449,9 +455,7 @@ def bench_b200(args, cfg):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded generator, DESIGN.md §6)",
         "config": {
-            "workload": f"{cfg.name}: {cfg.planes}x{cfg.h}x{cfg.w} "
-                        f"{'u8' if cfg.u8 else 'f32'}, {cfg.iters or 1} "
-                        f"{'iterations' if cfg.iters else 'map evaluation'}, dt={cfg.dt}",
+            "workload": workload_name(cfg),
             "iters": cfg.iters, "planes": cfg.planes, "h": cfg.h, "w": cfg.w,
             "sweeps_per_launch": 1 if cfg.iters == 0 else K,
             "parallelism": (f"rowband{world}" if cfg.sharding == "rows" and world > 1 else
@@ -503,13 +507,21 @@ def bench_reference(args, cfg):
     img = np.ascontiguousarray(full[:crop[0], :crop[1]], dtype=np.float64)
     if cfg.u8:
         img = img / 255.0
-    n_it = 1 if cfg.iters == 0 else 2
+    def run(n):
+        if cfg.iters == 0:
+            for _ in range(n):
+                oracle.wmc_map_f64(img, threads)
+        else:
+            oracle.flow_f64(img, n, cfg.dt, threads)
+    # a step = n iterations (map evaluations) on the crop, n sized to ~0.5 s
+    run(1)
+    t0 = time.perf_counter()
+    run(1)
+    one = max(time.perf_counter() - t0, 1e-6)
+    n_it = max(1, min(cfg.iters or 50, int(0.5 / one)))
 
     def sample():
-        if cfg.iters == 0:
-            oracle.wmc_map_f64(img, threads)
-        else:
-            oracle.flow_f64(img, n_it, cfg.dt, threads)
+        run(n_it)
     for _ in range(args.warmup):
         sample()
     t0 = time.perf_counter()
@@ -526,8 +538,9 @@ def bench_reference(args, cfg):
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak" if cfg.sharding == "images" else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generator, DESIGN.md §6)",
-        "config": {"workload": f"{cfg.name} (bounded CPU sample)", "iters": cfg.iters,
-                   "planes": cfg.planes, "h": cfg.h, "w": cfg.w},
+        "config": {"workload": workload_name(cfg), "iters": cfg.iters, "planes": cfg.planes,
+                   "h": cfg.h, "w": cfg.w, "parallelism": f"cpu{threads}",
+                   "sample": f"{crop[0]}x{crop[1]} crop, {n_it} iteration(s) per step"},
         "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": threads,
                          "kind": "port", "sample": desc},
         "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
