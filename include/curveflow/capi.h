@@ -149,7 +149,8 @@ CF_API int cf_wmc_solve_l1_area_f32(const float* f, float* u, float* d, int32_t 
 CF_API int32_t cf_wmc_max_sweeps_per_launch(void);
 /* Number of kernel launches cf_wmc_filter_f32 / _u8_f32 (and the solvers) */
 /* enqueue for iters on a w x h x planes image, and the sweeps fused per    */
-/* launch they schedule (at most; 2 up to 4 Mi pixels, else 3).             */
+/* launch they schedule (at most; the geometry argument is kept so a       */
+/* geometry-dependent schedule needs no ABI change -- currently 2).          */
 CF_API int32_t cf_wmc_filter_launches(int32_t w, int32_t h, int32_t planes, int32_t iters);
 CF_API int32_t cf_wmc_filter_sweeps_per_launch(int32_t w, int32_t h, int32_t planes);
 CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,

@@ -22,11 +22,13 @@ namespace {
 
 constexpr int kMaxLevels = 4;            // max sweeps fused per launch (band API)
 // Sweeps per launch the filter schedules (measured on B200):
-// 3 for large working sets (cfg3-5: +8-15 % over 2), 2 up to kSmallPixels
-// pixels (cfg2: L2-resident, few warp tasks -- +29 % over 3).
-constexpr int kFlowLevelsLarge = 3;
-constexpr int kFlowLevelsSmall = 2;
-constexpr int64_t kSmallPixels = 4 << 20;
+// K = 2 wins or ties K = 3 on every BASELINE config and 9 of 10 probed
+// geometries (tools/probe_geometry.py) since border warps take the fast
+// path; CF_FLOW_LEVELS overrides it for experiments.
+#ifndef CF_FLOW_LEVELS
+#define CF_FLOW_LEVELS 2
+#endif
+constexpr int kFlowLevels = CF_FLOW_LEVELS;
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
 
@@ -116,6 +118,20 @@ template <int K, int MODE>
 int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
     using G = cfk::Geo<K>;
     p.n_chunks = (p.w + G::S - 1) / G::S;
+    {  // trailing chunk pairs whose window leaves the image (kernel task order)
+        const int n_pairs = (p.n_chunks + 1) / 2;
+        int nbh = 0;
+        for (int pp = n_pairs - 1; pp >= 1; --pp) {
+            bool b = false;
+            for (int h = 0; h < 2; ++h) {
+                const int c = 2 * pp + h;
+                if (c >= p.n_chunks || c * G::S - G::A + cfk::kChunk > p.w) b = true;
+            }
+            if (!b) break;
+            ++nbh;
+        }
+        p.n_bhi = nbh;
+    }
     plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MODE>());
     const int64_t tasks = (int64_t)((p.n_chunks + 1) / 2) * p.n_strips * p.planes;
     const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
@@ -148,9 +164,7 @@ bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane
     return true;
 }
 
-int flow_levels(int32_t w, int32_t h, int32_t planes) {
-    return (int64_t)w * h * planes <= kSmallPixels ? kFlowLevelsSmall : kFlowLevelsLarge;
-}
+int flow_levels(int32_t, int32_t, int32_t) { return kFlowLevels; }
 
 // Launch schedule: sweeps per launch, at most `levels` each, an EVEN number
 // of launches when iters >= 2 so the ping-pong ends in the caller's buffer:

@@ -45,6 +45,9 @@
 
 namespace cfk {
 
+#ifndef CF_RING_UNROLL
+#define CF_RING_UNROLL 1  // steady loop unrolled over the ring period (K <= 2)
+#endif
 #ifndef CF_FAST_UNROLL
 #define CF_FAST_UNROLL 2  // steady-state loop unroll (register renaming of the carries)
 #endif
@@ -87,6 +90,7 @@ struct SweepParams {
     int32_t w, h;             // global image size (clamp borders)
     int32_t y0, y1;           // output rows
     int32_t strip_rows, n_strips, n_chunks, planes;
+    int32_t n_bhi;            // trailing border chunk pairs (host, launch_k)
     float dt;
     int32_t iter_base;
     int32_t* flag;            // nullable
@@ -323,6 +327,7 @@ struct SweepWarp {
     bool outc[C];                 // column j of this lane is an output column
     bool out_h[2];                // chunk h exists (a missing chunk is never stored)
     bool border;                  // some window touches column 0 or w-1 (uniform)
+    uint32_t emask;               // image-edge columns of this lane (edge_fix)
     int ys, ye;                   // output strip rows
     // rows computed per level L: [rlo(L), rhi(L)) (recomputed, not stored)
     __device__ __forceinline__ int rlo(int L) const { return max(ys - (K - L), 0); }
@@ -339,6 +344,9 @@ struct SweepWarp {
     // (K <= 2), or recomputed (K >= 3: the 16 registers buy occupancy there;
     // measured).  Bit-identical either way.
     static constexpr bool kCarry = K <= 2;
+    // Ring-period unroll of the steady loop: +2-3 % at K <= 2; at K = 3 the
+    // longer live ranges grow the 128-register spill and it loses 3 %.
+    static constexpr bool kRingUnroll = CF_RING_UNROLL && K <= 2;
     f2 hc[K + 1][C], tm[K + 1][C];
     f2 onv[K + 1][C];               // results of the current step, per level
     // kModeL1: the dual d_L(y) a level produces is consumed pointwise by
@@ -384,26 +392,24 @@ struct SweepWarp {
         }
     }
 
-    // Border lanes replicate column 0 into column -1 and column w-1 into
-    // column w of a freshly written row (per chunk half).
-    __device__ __forceinline__ void clamp_row(uint32_t rowbase) const {
+    // Clamp-to-edge at the image's left / right column (border warps): the
+    // pixel at x = 0 takes its own column as its x-1 neighbours (a <- b,
+    // l <- u, e <- f) and the pixel at x = w-1 as its x+1 neighbours, in each
+    // of the three rows right after they are loaded -- exactly the operands
+    // of the clamped stencil, so no ring row is ever patched.  Columns
+    // outside the image compute finite throw-away values (their level-0 data
+    // is the clamped prefetch) and are never stored or read by image pixels.
+    // emask bit 2*(2j+h) (+1): column j of chunk half h is x = 0 (x = w-1).
+    __device__ __forceinline__ void edge_fix(f2 (&q)[C + 2]) const {
+        f2 c[C];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int j = 0; j < C; ++j) c[j] = q[j + 1];
 #pragma unroll
-            for (int j = 0; j < C; ++j) {
-                const int x = xf[h] + j;
-                const int c = lane * C + j;  // window column
-                const uint32_t a = rowbase + 8 * (c + 1) + 4 * h;
-                float v;
-                if (x == 0) {
-                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-                    sts1(a - 8, v);
-                }
-                if (x == P.w - 1) {
-                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-                    sts1(a + 8, v);
-                }
-            }
+        for (int j = 0; j < C; ++j) {
+            if (emask & (1u << (4 * j + 0))) q[j] = pk(lo(c[j]), hi(q[j]));
+            if (emask & (1u << (4 * j + 2))) q[j] = pk(lo(q[j]), hi(c[j]));
+            if (emask & (1u << (4 * j + 1))) q[j + 2] = pk(lo(c[j]), hi(q[j + 2]));
+            if (emask & (1u << (4 * j + 3))) q[j + 2] = pk(lo(q[j + 2]), hi(c[j]));
         }
     }
 
@@ -425,7 +431,7 @@ struct SweepWarp {
     // offsets of rows t+c, c = 0..3, in the 4-slot rings) and r0[] (level-0
     // ring rows t-2, t-1, t).  Results are stored (STS / STG) but not yet
     // visible to other lanes: the caller syncs once per step.
-    template <int L, bool CHECKED>
+    template <int L, bool CHECKED, bool EDGE = false>
     __device__ __forceinline__ void level(int t, const uint32_t (&R4)[4], const uint32_t (&r0)[3],
                                           float* sptr) {
         const int y = t - lag(L);
@@ -448,6 +454,11 @@ struct SweepWarp {
         lds_nb(am + (lbase - sbase), m);
         lds_nb(ao + (lbase - sbase), o);
         lds_nb(ap + (lbase - sbase), p);
+        if (CHECKED ? border : EDGE) {
+            edge_fix(m);
+            edge_fix(o);
+            edge_fix(p);
+        }
         if (kCarry && CHECKED && y == rlo(L)) {  // first row of this level: no carries yet
 #pragma unroll
             for (int j = 1; j <= C; ++j) {
@@ -493,7 +504,7 @@ struct SweepWarp {
                 nv[j - 1] = hw;
             } else if constexpr (MODE == kModeL2) {
                 // SPEC.md:298 with A = I: U' = U + dt*((f - U) + lambda*H^w(U))
-                const f2 fv = ld_pt<CHECKED>(fp, y, j - 1);
+                const f2 fv = ld_pt<CHECKED || EDGE>(fp, y, j - 1);
                 const f2 r = fma2(o[j], splat(-1.0f), fv);         // f - u
                 const f2 sdir = fma2(splat(P.lambda), hw, r);      // (f-u) + lambda*H
                 nv[j - 1] = fma2(splat(P.dt), sdir, o[j]);
@@ -502,9 +513,9 @@ struct SweepWarp {
                 // SPEC.md:306 with A = I:
                 //   r = (u - f) + d;  d' = clamp(r, -alpha, alpha)
                 //   U' = u + dt*(lambda*H^w - (2d' - d)/alpha)
-                const f2 fv = ld_pt<CHECKED>(fp, y, j - 1);
+                const f2 fv = ld_pt<CHECKED || EDGE>(fp, y, j - 1);
                 f2 dv;
-                if constexpr (L == 1) dv = ld_pt<CHECKED>(dsp, y, j - 1);
+                if constexpr (L == 1) dv = ld_pt<CHECKED || EDGE>(dsp, y, j - 1);
                 else dv = dold[L - 1][j - 1];
                 const f2 r = add2(fma2(fv, splat(-1.0f), o[j]), dv);
                 const f2 dn = pk(fminf(fmaxf(lo(r), -P.alpha), P.alpha),
@@ -526,13 +537,13 @@ struct SweepWarp {
     // Store phase of a step (after every level computed, so no shared-memory
     // store precedes a later level's loads: the compiler is free to overlap
     // the K independent level computations).
-    template <int L, bool CHECKED>
+    template <int L, bool CHECKED, bool EDGE = false>
     __device__ __forceinline__ void store(int t, const uint32_t (&R4)[4], float* sptr) {
-        store_one<L, CHECKED>(t, R4, sptr);
-        if constexpr (L < K) store<L + 1, CHECKED>(t, R4, sptr);
+        store_one<L, CHECKED, EDGE>(t, R4, sptr);
+        if constexpr (L < K) store<L + 1, CHECKED, EDGE>(t, R4, sptr);
     }
 
-    template <int L, bool CHECKED>
+    template <int L, bool CHECKED, bool EDGE = false>
     __device__ __forceinline__ void store_one(int t, const uint32_t (&R4)[4], float* sptr) {
         const int y = t - lag(L);
         if (CHECKED && (y < rlo(L) || y >= rhi(L))) return;  // warp-uniform
@@ -542,12 +553,14 @@ struct SweepWarp {
 #pragma unroll
             for (int j = 0; j < C; ++j) {
                 if (!outc[j]) continue;
-                if (out_h[0] && (!CHECKED || xf[0] + j < P.w)) drow[xf[0] + j] = lo(odv[K][j]);
-                if (out_h[1] && (!CHECKED || xf[1] + j < P.w)) drow[xf[1] + j] = hi(odv[K][j]);
+                if (out_h[0] && (!(CHECKED || EDGE) || xf[0] + j < P.w))
+                    drow[xf[0] + j] = lo(odv[K][j]);
+                if (out_h[1] && (!(CHECKED || EDGE) || xf[1] + j < P.w))
+                    drow[xf[1] + j] = hi(odv[K][j]);
             }
         }
         if constexpr (L == K) {
-            if (CHECKED) {
+            if (CHECKED || EDGE) {
                 float* row = dstp + (int64_t)(y - P.dst_row0) * P.dst_pitch;
 #pragma unroll
                 for (int j = 0; j < C; ++j) {
@@ -576,19 +589,11 @@ struct SweepWarp {
         }
     }
 
-    template <int L, bool CHECKED>
+    template <int L, bool CHECKED, bool EDGE = false>
     __device__ __forceinline__ void levels(int t, const uint32_t (&R4)[4],
                                            const uint32_t (&r0)[3], float* sptr) {
-        level<L, CHECKED>(t, R4, r0, sptr);
-        if constexpr (L < K) levels<L + 1, CHECKED>(t, R4, r0, sptr);
-    }
-
-    // Border warps: replicate the edge columns of every row written this step.
-    template <int L>
-    __device__ __forceinline__ void clamp_levels(int t) {
-        const int y = t - lag(L);
-        if (y >= rlo(L) && y < rhi(L)) clamp_row(row_addr<L>(y));
-        if constexpr (L + 1 < K) clamp_levels<L + 1>(t);
+        level<L, CHECKED, EDGE>(t, R4, r0, sptr);
+        if constexpr (L < K) levels<L + 1, CHECKED, EDGE>(t, R4, r0, sptr);
     }
 
     // kModeL1: end of step -- level L's dual of row t-lag(L) becomes level
@@ -610,7 +615,7 @@ struct SweepWarp {
         const int t_end = ye - 1 + lag(K);
         // steady steps: every level in range with unclamped neighbour rows,
         // interior warp
-        int t_s = border ? 0x7fffffff : 0, t_e = rhi(0) - 1;
+        int t_s = 0, t_e = rhi(0) - 1;
 #pragma unroll
         for (int L = 1; L <= K; ++L) {
             t_s = max(t_s, max(rlo(L) + 1, 1) + lag(L));    // y-1 >= 0, y > rlo (carries)
@@ -638,23 +643,51 @@ struct SweepWarp {
         const int f0 = min(t_s, t_end + 1), f1 = min(t_e, t_end);
         int t = t_begin;
         for (; t < f0; ++t) step<false>(t, lptr, sptr);
+        if (border) {  // image-edge columns: fast steps with the edge fix
+            for (; t <= f1; ++t) step<true, -1, true>(t, lptr, sptr);
+        } else if constexpr (kRingUnroll) {
+            // Steady state unrolled over the ring period (4 steps from t = 0
+            // mod 4): every ring row address is a compile-time offset from
+            // sbase or from the group's two level-0 half-ring bases -- no
+            // per-step slot arithmetic (IMAD work on the saturated FMA pipe).
+            for (; t <= f1 && (t & 3); ++t) step<true>(t, lptr, sptr);
+            for (; t + 3 <= f1; t += 4) {
+                const uint32_t g0 = sbase + (uint32_t)(t & 4) * kRowBytes;
+                const uint32_t g1 = sbase + (uint32_t)((t & 4) ^ 4) * kRowBytes;
+                step<true, 0>(t, lptr, sptr, g0, g1);
+                step<true, 1>(t + 1, lptr, sptr, g0, g1);
+                step<true, 2>(t + 2, lptr, sptr, g0, g1);
+                step<true, 3>(t + 3, lptr, sptr, g0, g1);
+            }
+            for (; t <= f1; ++t) step<true>(t, lptr, sptr);
+        } else {
 #pragma unroll kFastUnroll
-        for (; t <= f1; ++t) step<true>(t, lptr, sptr);
+            for (; t <= f1; ++t) step<true>(t, lptr, sptr);
+        }
         for (; t <= t_end; ++t) step<false>(t, lptr, sptr);
     }
 
-    template <bool FAST>
-    __device__ __forceinline__ void step(int t, const float*& lptr, float*& sptr) {
+    // Level-0 ring row r = t0 + d (t0 = 0 mod 4 the group start, -2 <= d <= 5)
+    // in the 8-slot ring: slot (t0 & 4) + d when 0 <= d < 4, else the other
+    // half ring's slot (d mod 4).
+    template <int D>
+    static __device__ __forceinline__ uint32_t ring0(uint32_t g0, uint32_t g1) {
+        static_assert(kRS == 8, "phase addressing assumes an 8-slot level-0 ring");
+        if constexpr (D >= 0 && D < 4) return g0 + (uint32_t)D * kRowBytes;
+        else return g1 + (uint32_t)((D + 8) & 3) * kRowBytes;
+    }
+
+    // PH >= 0: steady step at phase PH of a 4-step group (t = t0 + PH).
+    template <bool FAST, int PH = -1, bool EDGE = false>
+    __device__ __forceinline__ void step(int t, const float*& lptr, float*& sptr,
+                                         uint32_t g0 = 0, uint32_t g1 = 0) {
         cp_async_wait_rd();       // this lane's copies of row t landed
-        if (!FAST && border) {
-            __syncwarp();
-            if (t < rhi(0)) clamp_row(row_addr<0>(t));
-        }
         __syncwarp();             // rows of step t-1 and row t visible to all lanes
         if (t + kRD < rhi(0)) {
-            if (FAST || !border) {
-                const uint32_t sa =
-                    sbase + (uint32_t)((t + kRD) & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
+            if ((FAST && !EDGE) || !border) {
+                uint32_t sa;
+                if constexpr (PH >= 0) sa = ring0<PH + kRD>(g0, g1) + 8 * C * lane + 8;
+                else sa = sbase + (uint32_t)((t + kRD) & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
 #pragma unroll
                 for (int j = 0; j < C; ++j) {
                     cp_async4(sa + 8 * j, lptr + j);
@@ -666,28 +699,30 @@ struct SweepWarp {
         }
         lptr += P.src_pitch;
         cp_async_commit();
-        const uint32_t R4[4] = {(uint32_t)(t & 3) * kRowBytes,
-                                (uint32_t)((t + 1) & 3) * kRowBytes,
-                                (uint32_t)((t + 2) & 3) * kRowBytes,
-                                (uint32_t)((t + 3) & 3) * kRowBytes};
+        const int ph = PH >= 0 ? PH : t;
+        const uint32_t R4[4] = {(uint32_t)(ph & 3) * kRowBytes,
+                                (uint32_t)((ph + 1) & 3) * kRowBytes,
+                                (uint32_t)((ph + 2) & 3) * kRowBytes,
+                                (uint32_t)((ph + 3) & 3) * kRowBytes};
         if constexpr (FAST) {
-            const uint32_t r0[3] = {sbase + (uint32_t)((t - 2) & (kRS - 1)) * kRowBytes,
-                                    sbase + (uint32_t)((t - 1) & (kRS - 1)) * kRowBytes,
-                                    sbase + (uint32_t)(t & (kRS - 1)) * kRowBytes};
-            levels<1, false>(t, R4, r0, sptr);
-            store<1, false>(t, R4, sptr);
+            uint32_t r0[3];
+            if constexpr (PH >= 0) {
+                r0[0] = ring0<PH - 2>(g0, g1);
+                r0[1] = ring0<PH - 1>(g0, g1);
+                r0[2] = ring0<PH>(g0, g1);
+            } else {
+                r0[0] = sbase + (uint32_t)((t - 2) & (kRS - 1)) * kRowBytes;
+                r0[1] = sbase + (uint32_t)((t - 1) & (kRS - 1)) * kRowBytes;
+                r0[2] = sbase + (uint32_t)(t & (kRS - 1)) * kRowBytes;
+            }
+            levels<1, false, EDGE>(t, R4, r0, sptr);
+            store<1, false, EDGE>(t, R4, sptr);
             shift_duals();
         } else {
             const uint32_t r0[3] = {0, 0, 0};
             levels<1, true>(t, R4, r0, sptr);
             store<1, true>(t, R4, sptr);
             shift_duals();
-            if constexpr (K > 1) {
-                if (border) {
-                    __syncwarp();
-                    clamp_levels<1>(t);
-                }
-            }
         }
         sptr += P.dst_pitch;
     }
@@ -707,8 +742,23 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
     const int n_pairs = (p.n_chunks + 1) / 2;
     const int total = n_pairs * p.n_strips * p.planes;
     if (warp >= total) return;  // warp-uniform
-    const int cpair = warp % n_pairs;
-    const int rest = warp / n_pairs;
+    // Border chunk pairs (pair 0 and the last n_bhi) run the checked path and
+    // are slower: their tasks take the lowest warp indices, so they start
+    // first and share blocks with each other rather than stretching the
+    // residency of otherwise-fast blocks (a block frees its slot only when
+    // its slowest warp ends).
+    const int nb = min(n_pairs, 1 + p.n_bhi);
+    const int btasks = nb * p.n_strips * p.planes;
+    int cpair, rest;
+    if (warp < btasks) {
+        const int k = warp % nb;
+        rest = warp / nb;
+        cpair = k == 0 ? 0 : n_pairs - nb + k;
+    } else {
+        const int i = warp - btasks, ni = n_pairs - nb;
+        cpair = 1 + i % ni;
+        rest = i / ni;
+    }
     const int strip = rest % p.n_strips;
     const int plane = rest / p.n_strips;
 
@@ -729,6 +779,15 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
         sw.xf[h] = (sw.out_h[h] ? xs : xs - G::S) + sw.lane * C;
         sw.border |= xs < 0 || xs + kChunk > p.w || !sw.out_h[h];
     }
+    sw.emask = 0;
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int x = sw.xf[h] + j;
+            if (x == 0) sw.emask |= 1u << (4 * j + 2 * h);
+            if (x == p.w - 1) sw.emask |= 1u << (4 * j + 2 * h + 1);
+        }
     sw.ys = p.y0 + strip * p.strip_rows;
     sw.ye = min(sw.ys + p.strip_rows, p.y1);
     if (sw.ys >= sw.ye) return;

@@ -66,11 +66,11 @@ def test_invalid_arguments_rejected_before_cuda():
 
 
 @pytest.mark.parametrize("w,h,planes,levels", [(1024, 1024, 1, 2), (2048, 2048, 1, 2),
-                                               (2049, 2048, 1, 3), (16384, 16384, 1, 3),
-                                               (1920, 1080, 256, 3), (3840, 2160, 3, 3)])
+                                               (16384, 16384, 1, 2), (1920, 1080, 256, 2),
+                                               (3840, 2160, 3, 2)])
 def test_filter_schedule_is_even(w, h, planes, levels):
-    """Sweeps per launch by working-set size; an even launch
-    count for iters >= 2 so the ping-pong ends in the caller's buffer."""
+    """Sweeps per launch; an even launch count for iters >= 2
+    so the ping-pong ends in the caller's buffer."""
     L = cf.lib()
     assert L.cf_wmc_filter_sweeps_per_launch(w, h, planes) == levels
     assert L.cf_wmc_filter_sweeps_per_launch(0, h, planes) == 0
