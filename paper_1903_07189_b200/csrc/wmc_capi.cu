@@ -97,7 +97,10 @@ int kernel_occupancy_warps() {
 void plan_strips(cfk::SweepParams& p, int K, int slots) {
     const int rows = p.y1 - p.y0;
     const int64_t per_strip_tasks = (int64_t)((p.n_chunks + 1) / 2) * p.planes;
-    const double overhead = (K - 1) + 6.0;  // warm-up rows + fixed per-task cost (rows)
+#ifndef CF_PLAN_OVH
+#define CF_PLAN_OVH 6.0
+#endif
+    const double overhead = (K - 1) + CF_PLAN_OVH;  // warm-up rows + fixed per-task cost (rows)
     const int max_strips = std::max(1, rows / std::max(8, 4 * K));
     double best_cost = 1e300;
     int best = 1;
