@@ -172,9 +172,18 @@ class ShardedFlow:
 
 
 def cuda_compute(flag=None) -> ComputeFn:
-    """Row-band kernel through the C-ABI (cf_wmc_sweeps_band_f32)."""
-    from .curveflow import sweeps_band
+    """Row-band kernel through the C-ABI (cf_wmc_sweeps_band_f32), on the
+    caller's current stream; a lean ctypes call (the sharded loop issues a
+    few of these per launch, so host cost per call matters at N = 8)."""
+    import torch
+
+    from ._lib import check, lib
+    fn_c = lib().cf_wmc_sweeps_band_f32
+    flag_ptr = flag.data_ptr() if flag is not None else None
 
     def fn(src, src_row0, dst, dst_row0, h, y0, y1, sweeps, dt, iter_base):
-        sweeps_band(src, src_row0, dst, dst_row0, h, y0, y1, sweeps, dt, iter_base, flag)
+        W = src.shape[1]
+        check(fn_c(src.data_ptr(), src_row0, src.shape[0], dst.data_ptr(), dst_row0, W, h, W, y0,
+                   y1, sweeps, float(dt), iter_base, flag_ptr,
+                   torch.cuda.current_stream().cuda_stream), "sweeps_band")
     return fn
