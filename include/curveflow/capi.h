@@ -135,6 +135,34 @@ CF_API int cf_wmc_solve_l1_area_f32(const float* f, float* u, float* d, int32_t 
                                     int32_t* first_bad_iter, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* Single-process sharded filter over P device buffers (SURVEY.md §8b      */
+/* export 4; BASELINE cfg 4 row bands).  The plan splits the h rows like    */
+/* the reference's parallel::for_rows (ceil-div blocks, parallel.hpp:36-44) */
+/* and gives each part k halo rows above / below (k = sweeps per launch,   */
+/* 1 <= k <= cf_wmc_max_sweeps_per_launch()).  Part p's buffers hold        */
+/* rows[p] x w floats (pitch w): global rows [row0-top, row1+bot); the      */
+/* caller places the band's owned rows at buffer row top[p] of bufs_a[p].   */
+/* Halo rows move between parts with cudaMemcpyPeerAsync (NVLink / NVSwitch */
+/* when the parts live on different GPUs), ordered by events, and each part */
+/* advances with the row-band kernel on streams[p] of devices[p].  The      */
+/* result is in bufs_a (an even number of launches); bit-identical to       */
+/* cf_wmc_filter_f32 for any P.  flags[p]: a device int32 on devices[p].    */
+/* first_bad_iter (nullable): synchronises all streams, as the filter.      */
+/* ---------------------------------------------------------------------- */
+#define CF_MAX_PARTS 64
+typedef struct {
+    int32_t h, w, parts, k;
+    int32_t row0[CF_MAX_PARTS], row1[CF_MAX_PARTS]; /* owned rows [row0, row1)   */
+    int32_t top[CF_MAX_PARTS], bot[CF_MAX_PARTS];   /* halo rows above / below   */
+    int32_t rows[CF_MAX_PARTS];                     /* buffer rows of each part  */
+} cf_shard_plan;
+CF_API int cf_shard_plan_init(int32_t h, int32_t w, int32_t parts, int32_t k, cf_shard_plan* plan);
+CF_API int cf_wmc_filter_sharded_f32(const cf_shard_plan* plan, float* const* bufs_a,
+                                     float* const* bufs_b, int32_t* const* flags,
+                                     const int32_t* devices, void* const* streams, int32_t iters,
+                                     float dt, int32_t* first_bad_iter);
+
+/* ---------------------------------------------------------------------- */
 /* Row-band primitive for sharded filtering (BASELINE cfg 4).               */
 /* Runs `sweeps` (1 <= sweeps <= cf_wmc_max_sweeps_per_launch()) Jacobi     */
 /* sweeps of the flow in ONE launch, producing global rows [y0, y1) of the  */

@@ -44,6 +44,8 @@ SIGNATURES = {
     "cf_wmc_solve_l1_area_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32, _i64]),
     "cf_wmc_solve_l1_area_f32": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32,
                                            _f32, _f32, _f32, _i32, _vp, _sz, _pi32, _vp]),
+    "cf_shard_plan_init": (C.c_int, [_i32, _i32, _i32, _i32, _vp]),
+    "cf_wmc_filter_sharded_f32": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f32, _pi32]),
     "cf_wmc_max_sweeps_per_launch": (_i32, []),
     "cf_wmc_filter_launches": (_i32, [_i32, _i32, _i32, _i32]),
     "cf_wmc_filter_sweeps_per_launch": (_i32, [_i32, _i32, _i32]),
@@ -67,6 +69,17 @@ SIGNATURES = {
     "cf_synth_u8": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_kernel_bank_x12": (None, [_pi32]),
 }
+
+
+CF_MAX_PARTS = 64
+
+
+class CfShardPlan(C.Structure):
+    """cf_shard_plan (include/curveflow/capi.h)."""
+    _fields_ = [("h", _i32), ("w", _i32), ("parts", _i32), ("k", _i32),
+                ("row0", _i32 * CF_MAX_PARTS), ("row1", _i32 * CF_MAX_PARTS),
+                ("top", _i32 * CF_MAX_PARTS), ("bot", _i32 * CF_MAX_PARTS),
+                ("rows", _i32 * CF_MAX_PARTS)]
 
 
 def lib():

@@ -170,7 +170,8 @@ bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane
 int flow_levels(int32_t, int32_t, int32_t) { return kFlowLevels; }
 
 // Launch schedule: sweeps per launch, at most `levels` each, an EVEN number
-// of launches when iters >= 2 so the ping-pong ends in the caller's buffer:
+// of launches when iters >= 2 (unless levels == 1 and iters is odd) so the
+// ping-pong ends in the caller's buffer:
 // n = the smallest even count >= ceil(iters / levels), sweeps spread evenly
 // (200 at 3 levels -> 64 x 3 + 4 x 2: no single-sweep launch, each of which
 // would cost a full HBM pass).
@@ -179,6 +180,7 @@ std::vector<int> schedule(int iters, int levels) {
     if (iters == 1) return {1};
     int n = (iters + levels - 1) / levels;
     n += n & 1;
+    n = std::min(n, iters);  // levels == 1, odd iters: odd count, callers copy back
     std::vector<int> ks(n, iters / n);
     for (int i = 0; i < iters % n; ++i) ks[i] += 1;
     return ks;
@@ -199,8 +201,14 @@ __global__ void u8_to_f32_kernel(const uint8_t* in, int64_t in_pitch, int64_t in
 
 }  // namespace
 
-// Shared with wmc_io.cu; hidden (not part of the C-ABI).
+// Shared with wmc_io.cu / wmc_shard.cpp; hidden (not part of the C-ABI).
 extern "C" void cf_internal_set_cuda_error(int e) { g_last_cuda = e; }
+extern "C" int cf_internal_schedule(int32_t iters, int32_t levels, int32_t* out, int32_t cap) {
+    const std::vector<int> ks = schedule(iters, levels);
+    if ((int32_t)ks.size() > cap) return -1;
+    for (size_t i = 0; i < ks.size(); ++i) out[i] = ks[i];
+    return (int32_t)ks.size();
+}
 
 extern "C" {
 

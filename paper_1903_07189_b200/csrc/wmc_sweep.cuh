@@ -62,7 +62,10 @@ constexpr int kFastUnroll = CF_FAST_UNROLL;
 #ifndef CF_MINB_EVEN
 #define CF_MINB_EVEN 3  // K = 2
 #endif
-constexpr int kWarpsPerBlock = 4;
+#ifndef CF_WPB
+#define CF_WPB 4
+#endif
+constexpr int kWarpsPerBlock = CF_WPB;
 constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kFull = 0xffffffffu;
 #ifndef CF_COLS

@@ -187,3 +187,63 @@ def cuda_compute(flag=None) -> ComputeFn:
                    y1, sweeps, float(dt), iter_base, flag_ptr,
                    torch.cuda.current_stream().cuda_stream), "sweeps_band")
     return fn
+
+
+def plan(h: int, w: int, parts: int, k: int):
+    """cf_shard_plan for the single-process sharded filter (C-ABI)."""
+    import ctypes as C
+
+    from ._lib import CfShardPlan, check, lib
+    pl = CfShardPlan()
+    check(lib().cf_shard_plan_init(h, w, parts, k, C.addressof(pl)), "cf_shard_plan_init")
+    return pl
+
+
+def filter_sharded(img, iters: int, dt: float = 1.0, parts: int = 2, devices=None, k=None,
+                   check_finite: bool = True):
+    """mc_flow of one image split into `parts` row bands on `devices` (one
+    process; cf_wmc_filter_sharded_f32: halos over cudaMemcpyPeerAsync).
+    img: (H, W) float32 torch tensor or numpy array; returns a tensor on the
+    first device (numpy for numpy input)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from ._lib import CF_ENONFINITE, check, lib
+    from .curveflow import FlowError
+    host = isinstance(img, np.ndarray)
+    x = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)) if host else img
+    H, W = x.shape
+    devices = list(devices) if devices is not None else [torch.cuda.current_device()] * parts
+    if len(devices) != parts:
+        raise ValueError("one device per part")
+    k = int(k) if k is not None else int(lib().cf_wmc_filter_sweeps_per_launch(W, H, 1))
+    pl = plan(H, W, parts, k)
+    bufs_a, bufs_b, flags, streams = [], [], [], []
+    for p in range(parts):
+        dev = torch.device("cuda", devices[p])
+        a = torch.zeros((pl.rows[p], W), dtype=torch.float32, device=dev)
+        a[pl.top[p]:pl.top[p] + pl.row1[p] - pl.row0[p]] = x[pl.row0[p]:pl.row1[p]].to(dev)
+        bufs_a.append(a)
+        bufs_b.append(torch.empty_like(a))
+        flags.append(torch.empty(1, dtype=torch.int32, device=dev))
+        streams.append(torch.cuda.current_stream(dev))
+    arr = lambda xs: (C.c_void_p * parts)(*[t.data_ptr() for t in xs])  # noqa: E731
+    pa, pb, pf = arr(bufs_a), arr(bufs_b), arr(flags)
+    pd = (C.c_int32 * parts)(*devices)
+    ps = (C.c_void_p * parts)(*[s.cuda_stream for s in streams])
+    bad = C.c_int32(0)
+    rc = lib().cf_wmc_filter_sharded_f32(C.addressof(pl), C.addressof(pa), C.addressof(pb),
+                                         C.addressof(pf), C.addressof(pd), C.addressof(ps),
+                                         int(iters), float(dt),
+                                         C.byref(bad) if check_finite else None)
+    if rc == CF_ENONFINITE:
+        raise FlowError(bad.value)
+    check(rc, "filter_sharded")
+    out = torch.empty((H, W), dtype=torch.float32, device=torch.device("cuda", devices[0]))
+    for p in range(parts):
+        band = bufs_a[p][pl.top[p]:pl.top[p] + pl.row1[p] - pl.row0[p]]
+        out[pl.row0[p]:pl.row1[p]] = band.to(out.device)
+    return out.cpu().numpy() if host else out
+

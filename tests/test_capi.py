@@ -140,3 +140,23 @@ def test_cpp_cli_built():
     assert os.access(exe, os.X_OK)
     r = __import__("subprocess").run([exe], capture_output=True, text=True)
     assert r.returncode == 2 and "usage" in r.stderr
+
+
+def test_shard_plan_follows_for_rows():
+    """cf_shard_plan_init: parallel.hpp:36 ceil-div bands, k halo rows."""
+    from paper_1903_07189_b200 import sharded
+    for h, parts, k in [(10, 4, 1), (16384, 8, 3), (100, 3, 2), (7, 1, 4)]:
+        pl = sharded.plan(h, 33, parts, k)
+        assert [(pl.row0[p], pl.row1[p]) for p in range(parts)] == sharded.band_bounds(h, parts)
+        for p in range(parts):
+            assert pl.top[p] == (k if p > 0 else 0) and pl.bot[p] == (k if p < parts - 1 else 0)
+            assert pl.rows[p] == pl.top[p] + pl.row1[p] - pl.row0[p] + pl.bot[p]
+    L = cf.lib()
+    import ctypes as C
+    from paper_1903_07189_b200._lib import CF_EINVAL as EINVAL, CfShardPlan
+    pl = CfShardPlan()
+    assert L.cf_shard_plan_init(3, 8, 4, 1, C.addressof(pl)) == EINVAL    # parts > h
+    assert L.cf_shard_plan_init(10, 8, 4, 3, C.addressof(pl)) == EINVAL   # band < k rows
+    assert L.cf_shard_plan_init(10, 8, 2, 9, C.addressof(pl)) == EINVAL   # k > max sweeps
+    assert L.cf_shard_plan_init(10, 8, 65, 1, C.addressof(pl)) == EINVAL  # > CF_MAX_PARTS
+    assert L.cf_wmc_filter_sharded_f32(None, None, None, None, None, None, 3, 1.0, None) == EINVAL

@@ -413,3 +413,25 @@ def test_sharded_overlap_streams_on_one_gpu(world, iters):
         t.join(timeout=300)
     assert not errs, errs
     assert_bitexact(out, ref, f"sharded world={world}")
+
+
+@pytest.mark.parametrize("h,w,parts,k,iters", [(64, 100, 2, 2, 7), (150, 233, 3, 3, 20),
+                                               (97, 61, 5, 2, 1), (40, 300, 4, 4, 9),
+                                               (33, 17, 1, 2, 6), (120, 129, 8, 1, 5)])
+def test_filter_sharded_single_process(h, w, parts, k, iters):
+    """cf_wmc_filter_sharded_f32 (SURVEY §8b export 4): P row bands with
+    cudaMemcpyPeerAsync halos (all parts on this GPU) == the single filter."""
+    from paper_1903_07189_b200 import sharded
+    img = cf.synth_image(h, w, seed=h + parts, n_rects=5, n_discs=5, sigma=0.1)
+    ref, _ = oracle.flow_f32(img, iters, 1.0)
+    got = sharded.filter_sharded(img, iters, parts=parts, k=k)
+    assert_bitexact(got, ref, f"sharded P={parts} k={k}")
+
+
+def test_filter_sharded_nonfinite_names_iteration():
+    from paper_1903_07189_b200 import sharded
+    img = cf.synth_image(90, 70, seed=4, n_rects=3, n_discs=3, sigma=0.1)
+    img[80, 10] = np.nan          # in the last band
+    with pytest.raises(cf.FlowError) as e:
+        sharded.filter_sharded(img, 6, parts=3, k=2)
+    assert e.value.iteration == 1
