@@ -435,3 +435,53 @@ def test_filter_sharded_nonfinite_names_iteration():
     with pytest.raises(cf.FlowError) as e:
         sharded.filter_sharded(img, 6, parts=3, k=2)
     assert e.value.iteration == 1
+
+
+def test_fuzz_random_geometries():
+    """Seeded random sweep over the filter's input space: shapes 1..300 x
+    1..700, 1-4 planes, padded pitches, iters 1..23, dt in (0, 1], value
+    scales; every case bit-exact vs the fp32 oracle (map and flow)."""
+    rng = np.random.default_rng(20261019)
+    for case in range(40):
+        h, w = int(rng.integers(1, 301)), int(rng.integers(1, 701))
+        P = int(rng.integers(1, 5))
+        pad = int(rng.integers(0, 40))
+        iters = int(rng.integers(1, 24))
+        dt = float(np.float32(rng.uniform(0.05, 1.0)))
+        scale = float(10.0 ** rng.uniform(-3, 3))
+        img = (rng.random((P, h, w)) * scale).astype(np.float32)
+        if case % 3 == 0:  # piecewise-constant structure: exact ties
+            img = np.round(img * 4 / scale).astype(np.float32) * np.float32(scale / 4)
+        d = torch.zeros((P, h, w + pad), dtype=torch.float32, device="cuda")
+        d[:, :, :w] = torch.from_numpy(img).cuda()
+        view = d[:, :, :w]
+        L = cf.lib()
+        stream = torch.cuda.current_stream().cuda_stream
+        assert_bitexact(cf.wmc_half_laplace(view.contiguous()).cpu().numpy(),
+                        oracle.wmc_map_f32(img), f"fuzz map case {case}")
+        nbytes = int(L.cf_wmc_filter_workspace_bytes(w, h, w + pad, P, h * (w + pad)))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        rc = L.cf_wmc_filter_f32(d.data_ptr(), w, h, w + pad, P, h * (w + pad), iters, dt,
+                                 ws.data_ptr(), nbytes, None, stream)
+        assert rc == 0, rc
+        ref, bad = oracle.flow_f32(img, iters, dt)
+        assert bad == 0
+        assert_bitexact(d[:, :, :w].cpu().numpy(), ref,
+                        f"fuzz flow case {case} ({P}x{h}x{w} pad {pad} it {iters} dt {dt})")
+        assert not d[:, :, w:].any(), "pitch padding written"
+
+
+def test_fuzz_nonfinite_positions():
+    """NaN / Inf injected at random pixels (borders included) and random
+    iteration counts: the reported first bad iteration equals the oracle's."""
+    rng = np.random.default_rng(7)
+    for case in range(12):
+        h, w = int(rng.integers(3, 200)), int(rng.integers(3, 400))
+        img = cf.synth_image(h, w, seed=case, n_rects=4, n_discs=4, sigma=0.1)
+        y, x = int(rng.integers(0, h)), int(rng.integers(0, w))
+        img[y, x] = [np.nan, np.inf, -np.inf][case % 3]
+        iters = int(rng.integers(1, 12))
+        _, bad = oracle.flow_f32(img, iters, 1.0)
+        with pytest.raises(cf.FlowError) as e:
+            cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(iters=iters))
+        assert e.value.iteration == bad == 1
