@@ -561,21 +561,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg4")
-    ap.add_argument("--all", default=None, help="run every config at N=1, write JSON lines")
+    ap.add_argument("--all", default=None, help="run every config (+ the supplemental 16384^2 "
+                    "map) at N=1, write JSON lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    from paper_1903_07189_b200.configs import CONFIGS
+    from paper_1903_07189_b200.configs import CONFIGS, SUPPLEMENTAL
     if args.all:
         with open(args.all, "w") as f:
-            for name in CONFIGS:
-                r = bench_b200(args, CONFIGS[name])
+            for name, c in list(CONFIGS.items()) + list(SUPPLEMENTAL.items()):
+                r = bench_b200(args, c)
                 if r:
                     f.write(json.dumps(r) + "\n")
                     f.flush()
                     print(json.dumps(r), flush=True)
         return
-    cfg = CONFIGS[args.workload]
+    cfg = {**CONFIGS, **SUPPLEMENTAL}[args.workload]
     res = bench_reference(args, cfg) if args.impl == "reference" else bench_b200(args, cfg)
     if res is not None:
         print(json.dumps(res), flush=True)

@@ -32,7 +32,7 @@ class WmcConfig:
         return self.pixels * max(1, self.iters)
 
     def seed(self, plane: int) -> int:
-        idx = int(self.name[3:])
+        idx = int(self.name[3:].split("_")[0])
         return SEED_BASE + 1000 * idx + plane
 
 
@@ -43,3 +43,11 @@ CONFIGS = {
     "cfg4": WmcConfig("cfg4", 16384, 16384, 1, 200, 2000, 2000, 0.10, sharding="rows"),
     "cfg5": WmcConfig("cfg5", 1920, 1080, 256, 20, 20, 20, 0.10, u8=True, sharding="images"),
 }
+
+# Not a BASELINE config: the map's HBM-roofline measurement on a large image
+# (cfg1 is L2-resident and launch-bound, so the stencil's HBM
+# claim comes from a supplemental 16384^2 single evaluation, cfg1's generator).
+SUPPLEMENTAL = {
+    "cfg1_16k": WmcConfig("cfg1_16k", 16384, 16384, 1, 0, 2000, 2000, 0.05),
+}
+

@@ -280,39 +280,47 @@ __device__ __forceinline__ f2 select_pair(const PairD& P) {
 
 // ---- fp64 near-tie resolution (MAP only) -------------------
 // Opposite-sign near tie: some D_j with D_j + D_m ~ 0 while |D_m| is not ~0.
-__device__ __forceinline__ bool near_tie(const PairD& P, int half, float best) {
-    float T = 3.0e38f;
+__device__ __forceinline__ void near_tie_pair(const PairD& P, f2 best, bool& t0, bool& t1) {
+    // T = min_k |fl(D_k + D_m)| per pixel; the sums are packed (FADD2), the
+    // magnitude minimum is fused into 3-input FMNMX3 by ptxas.
+    float T0 = 3.0e38f, T1 = 3.0e38f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const float dk = half ? hi(P.d[k]) : lo(P.d[k]);
-        T = fminf(T, fabsf(__fadd_rn(dk, best)));
+        const f2 sk = add2(P.d[k], best);
+        T0 = fminf(T0, fabsf(lo(sk)));
+        T1 = fminf(T1, fabsf(hi(sk)));
     }
-    const float n12u = half ? hi(P.n12u) : lo(P.n12u);
-    const float tau = __fmaf_rn(fabsf(n12u), 0x1.8p-19f, __fmul_rn(fabsf(best), 0x1.0p-20f));
-    return T <= tau && T < fabsf(best);
+    const float b0 = lo(best), b1 = hi(best);
+    const float tau0 = __fmaf_rn(fabsf(lo(P.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b0), 0x1.0p-20f));
+    const float tau1 = __fmaf_rn(fabsf(hi(P.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b1), 0x1.0p-20f));
+    t0 = T0 <= tau0 && T0 < fabsf(b0);
+    t1 = T1 <= tau1 && T1 < fabsf(b1);
 }
 
 // SPEC-faithful fp64 evaluation of one pixel (oracle/wmc_px.h wmc_px_f64):
 // weights n/12 as double, taps in row-major order, s = s + w*x unfused,
 // strict-< first-minimum scan.
+// fp64 weights n/12 of h1..h8 (row-major taps), rounded once: the constant
+// n / 12.0 folded by the compiler is the IEEE quotient __ddiv_rn(n, 12.0).
+__device__ __constant__ double kH64[8][9] = {
+    {2 / 12.0, 2 / 12.0, 0.0, 4 / 12.0, -1.0, 0.0, 2 / 12.0, 2 / 12.0, 0.0},
+    {2 / 12.0, 4 / 12.0, 2 / 12.0, 2 / 12.0, -1.0, 2 / 12.0, 0.0, 0.0, 0.0},
+    {0.0, 2 / 12.0, 2 / 12.0, 0.0, -1.0, 4 / 12.0, 0.0, 2 / 12.0, 2 / 12.0},
+    {0.0, 0.0, 0.0, 2 / 12.0, -1.0, 2 / 12.0, 2 / 12.0, 4 / 12.0, 2 / 12.0},
+    {2 / 12.0, 4 / 12.0, 1 / 12.0, 4 / 12.0, -1.0, 0.0, 1 / 12.0, 0.0, 0.0},
+    {1 / 12.0, 4 / 12.0, 2 / 12.0, 0.0, -1.0, 4 / 12.0, 0.0, 0.0, 1 / 12.0},
+    {0.0, 0.0, 1 / 12.0, 0.0, -1.0, 4 / 12.0, 1 / 12.0, 4 / 12.0, 2 / 12.0},
+    {1 / 12.0, 0.0, 0.0, 4 / 12.0, -1.0, 0.0, 2 / 12.0, 4 / 12.0, 1 / 12.0}};
+
 __device__ __noinline__ float wmc_px_f64(float a, float b, float c, float l, float u, float r,
                                           float e, float f, float g) {
-    constexpr signed char H12[8][9] = {
-        {2, 2, 0, 4, -12, 0, 2, 2, 0}, {2, 4, 2, 2, -12, 2, 0, 0, 0},
-        {0, 2, 2, 0, -12, 4, 0, 2, 2}, {0, 0, 0, 2, -12, 2, 2, 4, 2},
-        {2, 4, 1, 4, -12, 0, 1, 0, 0}, {1, 4, 2, 0, -12, 4, 0, 0, 1},
-        {0, 0, 1, 0, -12, 4, 1, 4, 2}, {1, 0, 0, 4, -12, 0, 2, 4, 1}};
     const double x[9] = {a, b, c, l, u, r, e, f, g};
     double best = 0.0;
 #pragma unroll 1
     for (int i = 0; i < 8; ++i) {
         double s = 0.0;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            const int n = H12[i][t];
-            const double wgt = n == 0 ? 0.0 : (n == -12 ? -1.0 : __ddiv_rn((double)n, 12.0));
-            s = __dadd_rn(s, __dmul_rn(wgt, x[t]));
-        }
+        for (int t = 0; t < 9; ++t) s = __dadd_rn(s, __dmul_rn(kH64[i][t], x[t]));
         if (i == 0 || fabs(s) < fabs(best)) best = s;
     }
     return __double2float_rn(best);
@@ -493,7 +501,8 @@ struct SweepWarp {
             const f2 b = select_pair(D);
             f2 hw = mul2(b, kC12x2);
             if constexpr (MAP) {
-                const bool t0 = near_tie(D, 0, lo(b)), t1 = near_tie(D, 1, hi(b));
+                bool t0, t1;
+                near_tie_pair(D, b, t0, t1);
                 if (__any_sync(kFull, t0 | t1)) {
                     float h0 = lo(hw), h1 = hi(hw);
                     if (t0) h0 = wmc_px_f64(lo(m[j - 1]), lo(m[j]), lo(m[j + 1]), lo(o[j - 1]),
