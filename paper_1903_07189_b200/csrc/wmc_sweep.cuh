@@ -20,14 +20,20 @@
 //    selection (FSETP+FSEL) is scalar.
 //  * Rows live in warp-private SHARED MEMORY, not registers: level 0 in a
 //    ring filled RD rows ahead by cp.async (4-byte copies land interleaved
-//    as pairs), levels 1..K-1 in 3-row rings written by the producing level.
+//    as pairs), levels 1..K-1 in 4-row rings written by the producing level.
 //    A lane reads its 4-column neighbourhood of a row with two 16-byte LDS
 //    (halo columns come from the neighbour lanes' slots -- no shuffles), so
-//    registers hold only the pixels in flight (~100 regs, high occupancy)
-//    and K can grow without register cost.
+//    registers hold only the pixels in flight and the levels' row sums.
+//  * Skewed level pipeline: level L at step t computes row t - (2L - 1), so
+//    the K level computations of a step are independent; ring stores are
+//    deferred to the end of the step.  Three step loops (checked prologue,
+//    fast steady state, checked epilogue); at K <= 2 the steady loop is
+//    unrolled over the ring period so every ring address is an immediate.
 //  * Clamp-to-edge is applied to the CURRENT iterate at every
-//    level: rows by clamping the row index of the slot read, columns by the
-//    border lanes writing the replicated value into the halo slot.
+//    level: rows by clamping the row index of the slot read (checked steps),
+//    columns by an operand fix right after the row loads (edge_fix), so
+//    border warps run the fast steady loop too.  Border warps take the
+//    lowest warp indices (they start first and share blocks).
 //  * Non-finite check: one FFMA2 per pixel pair per level into
 //    a per-level accumulator (x*0 + acc is NaN iff x is not finite); the
 //    first level whose accumulator is NaN is atomically min-ed into a device
@@ -425,7 +431,8 @@ struct SweepWarp {
     }
 
     // Pointwise pair {plane[y][xf[0]+jj], plane[y][xf[1]+jj]} of an f-geometry
-    // plane (data term / dual); CHECKED clamps the columns of border warps.
+    // plane (data term / dual); CHECKED clamps the columns (checked steps and
+    // the border warps' edge steps).
     template <bool CHECKED>
     __device__ __forceinline__ f2 ld_pt(const float* plane, int y, int jj) const {
         const float* row = plane + (int64_t)y * P.f_pitch;
@@ -742,7 +749,7 @@ struct SweepWarp {
 
 template <int K, int MODE>
 // The solver modes carry f (and the dual FIFO): 3 blocks/SM = 168 registers,
-// no spills at K = 3.
+// no spills at the filter's K = 2.
 __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
                                            : (MODE == kModeFlow && K == 2)     ? CF_MINB_EVEN
                                                                                : CF_MINB)
@@ -754,11 +761,11 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
     const int n_pairs = (p.n_chunks + 1) / 2;
     const int total = n_pairs * p.n_strips * p.planes;
     if (warp >= total) return;  // warp-uniform
-    // Border chunk pairs (pair 0 and the last n_bhi) run the checked path and
-    // are slower: their tasks take the lowest warp indices, so they start
-    // first and share blocks with each other rather than stretching the
-    // residency of otherwise-fast blocks (a block frees its slot only when
-    // its slowest warp ends).
+    // Border chunk pairs (pair 0 and the last n_bhi) do extra per-step work
+    // (edge fix, clamped prefetch): their tasks take the lowest warp indices,
+    // so they start first and share blocks with each other rather than
+    // stretching the residency of otherwise-fast blocks (a block frees its
+    // slot only when its slowest warp ends).
     const int nb = min(n_pairs, 1 + p.n_bhi);
     const int btasks = nb * p.n_strips * p.planes;
     int cpair, rest;
