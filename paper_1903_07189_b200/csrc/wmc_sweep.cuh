@@ -686,13 +686,15 @@ struct SweepWarp {
         for (; t <= t_end; ++t) step<false>(t, lptr, sptr);
     }
 
-    // Level-0 ring row r = t0 + d (t0 = 0 mod 4 the group start, -2 <= d <= 5)
-    // in the 8-slot ring: slot (t0 & 4) + d when 0 <= d < 4, else the other
-    // half ring's slot (d mod 4).
+    // Level-0 ring row t0 + D (t0 = 0 mod 4 the group start, -2 <= D <= 8)
+    // in the 8-slot ring: slot ((t0 & 4) + D) & 7, i.e. the group's own half
+    // ring (g0) when bit 2 of D is clear (D = 0..3, 8) and the other half
+    // (g1) when it is set (D = -2, -1, 4..7), at offset D & 3.
     template <int D>
     static __device__ __forceinline__ uint32_t ring0(uint32_t g0, uint32_t g1) {
         static_assert(kRS == 8, "phase addressing assumes an 8-slot level-0 ring");
-        if constexpr (D >= 0 && D < 4) return g0 + (uint32_t)D * kRowBytes;
+        static_assert(D >= -4 && D < 12, "row outside the ring's reach");
+        if constexpr ((((D + 8) >> 2) & 1) == 0) return g0 + (uint32_t)((D + 8) & 3) * kRowBytes;
         else return g1 + (uint32_t)((D + 8) & 3) * kRowBytes;
     }
 

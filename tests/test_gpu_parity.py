@@ -485,3 +485,41 @@ def test_fuzz_nonfinite_positions():
         with pytest.raises(cf.FlowError) as e:
             cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(iters=iters))
         assert e.value.iteration == bad == 1
+
+
+def test_plane_beyond_int32_elements():
+    """A 65536 x 33000 plane (2.16e9 elements > 2^31, 8.6 GB): the filter's
+    64-bit addressing.  Rows past element 2^31 are checked against the oracle
+    on a crop with iters halo rows (Jacobi locality: the crop interior is
+    exact), plus the first and last rows (clamp at both image edges)."""
+    w, h, iters = 65536, 33000, 3
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand((h, w), device="cuda", generator=g)
+    y0 = (1 << 31) // w + 7          # first checked row: past element 2^31
+    crops = [(0, 6), (y0, y0 + 6), (h - 6, h)]
+    inputs = {c: x[max(0, c[0] - iters):min(h, c[1] + iters)].cpu().numpy() for c in crops}
+    cf.mc_flow(x, cf.FlowConfig(iters=iters), inplace=True)
+    for (a, b), src in inputs.items():
+        ref, bad = oracle.flow_f32(src, iters, 1.0)
+        assert bad == 0
+        off = a - max(0, a - iters)
+        want = ref[off:off + (b - a)]
+        assert_bitexact(x[a:b].cpu().numpy(), want, f"rows {a}:{b}")
+    del x
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("P,h,w,iters", [(1, 300, 65536, 10), (60, 512, 1024, 7),
+                                         (3, 2160, 3840, 4), (1, 4000, 16384, 2)])
+def test_long_strips_bitexact(P, h, w, iters):
+    """Geometries whose strip planner picks LONG strips (hundreds of rows per
+    warp task), so the steady loop runs many ring periods and every prefetch
+    phase: the small-image tests get ~8-row strips and never reach the
+    steady state's later phases (a ring-slot bug there once went unseen)."""
+    g = torch.Generator(device="cuda").manual_seed(P * 7 + h)
+    x = torch.rand((P, h, w), device="cuda", generator=g)
+    src = x.cpu().numpy()
+    out = cf.mc_flow(x, cf.FlowConfig(iters=iters)).cpu().numpy()
+    ref, bad = oracle.flow_f32(src, iters, 1.0)
+    assert bad == 0
+    assert_bitexact(out, ref, f"long strips {P}x{h}x{w} it {iters}")
