@@ -523,3 +523,49 @@ def test_long_strips_bitexact(P, h, w, iters):
     ref, bad = oracle.flow_f32(src, iters, 1.0)
     assert bad == 0
     assert_bitexact(out, ref, f"long strips {P}x{h}x{w} it {iters}")
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_long_strips_band_api_every_k(k):
+    """Every fused depth through the band API on a geometry with long strips
+    (the N > 1 bench runs K = 3 bands of ~2000 rows)."""
+    h, w = 2100, 8192
+    g = torch.Generator(device="cuda").manual_seed(k)
+    x = torch.rand((h, w), device="cuda", generator=g)
+    y = torch.empty_like(x)
+    cf.sweeps_band(x, 0, y, 0, h, 0, h, k, 1.0, 0)
+    ref, _ = oracle.flow_f32(x.cpu().numpy(), k, 1.0)
+    assert_bitexact(y.cpu().numpy(), ref, f"band K={k}")
+
+
+def test_long_strips_map():
+    """The map kernel (K = 1, near-tie rule) on long strips."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand((2, 1200, 20000), device="cuda", generator=g)
+    assert_bitexact(cf.wmc_half_laplace(x).cpu().numpy(), oracle.wmc_map_f32(x.cpu().numpy()),
+                    "map long strips")
+
+
+@pytest.mark.parametrize("model", ["l1_area", "l2_area"])
+def test_long_strips_solvers(model):
+    f = np.stack([cf.synth_image(900, 9000, seed=s, n_rects=40, n_discs=40, sigma=0.1)
+                  for s in range(2)])
+    cfg = cf.SolverConfig(model=model, lam=2.0, alpha=0.2, iters=6)
+    rep = cf.solve(torch.from_numpy(f).cuda(), cfg)
+    if model == "l1_area":
+        ref, ref_d, bad = oracle.solve_l1_area_f32(f, 6, 0.15, 2.0, 0.2)
+        assert_bitexact(rep.dual.cpu().numpy(), ref_d, "l1 dual long strips")
+    else:
+        ref, bad = oracle.solve_l2_area_f32(f, 6, 0.15, 2.0)
+    assert bad == 0
+    assert_bitexact(rep.image.cpu().numpy(), ref, f"{model} long strips")
+
+
+def test_long_strips_u8_frames():
+    """cfg5-shaped frames (1080 x 1920, many planes -> long strips), u8 in and out."""
+    rng = np.random.default_rng(11)
+    q = rng.integers(0, 256, (24, 1080, 1920), dtype=np.uint8)
+    got = cf.mc_flow_u8(torch.from_numpy(q).cuda(), cf.FlowConfig(iters=4),
+                        out_dtype="u8").cpu().numpy()
+    ref, bad = oracle.flow_f32(oracle.u8_to_f32(q), 4, 1.0)
+    assert bad == 0 and np.array_equal(got, oracle.quantize_u8(ref))
