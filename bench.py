@@ -321,6 +321,26 @@ def bench_b200(args, cfg):
         rc = L.cf_wmc_filter_query_nonfinite((flag_ws if cfg.u8 else ws).data_ptr(),
                                              ctypes.byref(bad), sp)
         assert rc == 0, f"non-finite value in the timed run (iteration {bad.value})"
+    # Self-check (no oracle here): the timed output must equal, bit for bit,
+    # the same filter run as band launches of a different depth -- another
+    # steady-loop instantiation and schedule (any schedule gives the same
+    # Jacobi iterates).  f32 single-GPU configs; tests cover the rest.
+    selfcheck = None
+    if world == 1 and cfg.iters > 0 and not cfg.u8:
+        k_alt = 3 if K != 3 else 2
+        cur = dev_in.reshape(P, H, W).clone()
+        nxt = torch.empty_like(cur)
+        it = 0
+        for kk in sharded.launch_schedule(cfg.iters, k_alt):
+            for pl in range(P):
+                cf.sweeps_band(cur[pl], 0, nxt[pl], 0, H, 0, H, kk, cfg.dt, it)
+            cur, nxt = nxt, cur
+            it += kk
+        same = bool(torch.equal(cur.view(torch.int32), work.reshape(P, H, W).view(torch.int32)))
+        selfcheck = {"reference": f"band launches of {k_alt} sweeps (no oracle)",
+                     "bitwise_equal": same}
+        assert same, "self-check failed: the timed output differs from an alternative schedule"
+        del cur, nxt
     updates_job = cfg.updates  # whole job over all ranks (strong scaling for rows)
     if world > 1 and cfg.sharding == "images":
         updates_job = updates_local * world  # per-rank fixed share (weak scaling)
@@ -478,6 +498,7 @@ def bench_b200(args, cfg):
                              "double-buffered against the compute stream" if pipelined else
                              "sequential H2D, filter, D2H")},
         "gpu_launches": launches_per_step * args.steps,
+        "selfcheck": selfcheck,
         "clocks": clk.summary(),
     }
     if kern_ms is not None:
