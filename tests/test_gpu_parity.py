@@ -569,3 +569,45 @@ def test_long_strips_u8_frames():
                         out_dtype="u8").cpu().numpy()
     ref, bad = oracle.flow_f32(oracle.u8_to_f32(q), 4, 1.0)
     assert bad == 0 and np.array_equal(got, oracle.quantize_u8(ref))
+
+
+def test_plane_stride_with_gaps():
+    """plane_stride > pitch * h (C-ABI allows gaps between planes): planes are
+    read and written at their strides, the gaps stay untouched."""
+    P, h, w, pitch, iters = 3, 77, 130, 150, 9
+    stride = pitch * h + 1000
+    img = np.stack([cf.synth_image(h, w, seed=50 + p, n_rects=6, n_discs=6, sigma=0.1)
+                    for p in range(P)])
+    flat = torch.full((P * stride,), 7.0, dtype=torch.float32, device="cuda")
+    for p in range(P):
+        flat[p * stride:p * stride + h * pitch].view(h, pitch)[:, :w] = torch.from_numpy(img[p])
+    L = cf.lib()
+    nbytes = int(L.cf_wmc_filter_workspace_bytes(w, h, pitch, P, stride))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    assert L.cf_wmc_filter_f32(flat.data_ptr(), w, h, pitch, P, stride, iters, 1.0,
+                               ws.data_ptr(), nbytes, None,
+                               torch.cuda.current_stream().cuda_stream) == 0
+    ref, _ = oracle.flow_f32(img, iters, 1.0)
+    for p in range(P):
+        plane = flat[p * stride:p * stride + h * pitch].view(h, pitch)
+        assert_bitexact(plane[:, :w].cpu().numpy(), ref[p], f"plane {p}")
+        assert torch.all(plane[:, w:] == 7.0)
+        if p < P - 1:
+            assert torch.all(flat[p * stride + h * pitch:(p + 1) * stride] == 7.0)
+
+
+def test_concurrent_streams():
+    """Re-entrancy: filters on two streams at once, each with its
+    own workspace, each bit-exact."""
+    imgs = [cf.synth_image(600, 5000, seed=s, n_rects=30, n_discs=30, sigma=0.1)
+            for s in (1, 2)]
+    refs = [oracle.flow_f32(a, 12, 1.0)[0] for a in imgs]
+    streams = [torch.cuda.Stream() for _ in imgs]
+    outs = []
+    for a, s in zip(imgs, streams):
+        with torch.cuda.stream(s):
+            d = torch.from_numpy(a).cuda(non_blocking=False)
+            outs.append(cf.mc_flow(d, cf.FlowConfig(iters=12), inplace=True, check_finite=False))
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert_bitexact(o.cpu().numpy(), r, "concurrent stream")
