@@ -6,6 +6,7 @@
 // reference ships no code for them): wmc_half_laplace SPEC.md:171-179,
 // mc_flow(scheme=half_laplace) SPEC.md:256-272.
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
@@ -75,21 +76,25 @@ constexpr size_t smem_bytes() {
 
 template <int K, int MODE>
 int kernel_occupancy_warps() {
-    static int cached = -1;  // per instantiation; identical on every B200
-    if (cached < 0) {
+    // per instantiation; identical on every B200.  Atomic: first calls may
+    // come from several host threads at once (the ABI is re-entrant); they
+    // compute the same value.
+    static std::atomic<int> cached{-1};
+    int v = cached.load(std::memory_order_acquire);
+    if (v < 0) {
         if (smem_bytes<K>() > 48 * 1024)
             cudaFuncSetAttribute(cfk::wmc_sweeps_kernel<K, MODE>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<K>());
         int blocks = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks, cfk::wmc_sweeps_kernel<K, MODE>, cfk::kThreads,
-                smem_bytes<K>()) !=
+                &blocks, cfk::wmc_sweeps_kernel<K, MODE>, cfk::kThreads, smem_bytes<K>()) !=
                 cudaSuccess ||
             blocks <= 0)
             blocks = 2;
-        cached = blocks * cfk::kWarpsPerBlock;
+        v = blocks * cfk::kWarpsPerBlock;
+        cached.store(v, std::memory_order_release);
     }
-    return cached;
+    return v;
 }
 
 // Strip planner: choose rows per warp-task so that the number of waves times
