@@ -163,6 +163,37 @@ CF_API int cf_wmc_filter_sharded_f32(const cf_shard_plan* plan, float* const* bu
                                      float dt, int32_t* first_bad_iter);
 
 /* ---------------------------------------------------------------------- */
+/* Fused-halo row bands across processes.  As              */
+/* cf_wmc_sweeps_band_f32, and the launch also stores level-K rows          */
+/* y < peer_up_end into peer_up (the upper neighbour's destination buffer,  */
+/* whose row 0 is global row peer_up_row0) and rows y >= peer_dn_begin into */
+/* peer_dn: the halo exchange is part of the compute kernel's stores (peer  */
+/* memory mapped with cf_ipc_open_mem; NVLink between GPUs).  Null peers:   */
+/* identical to cf_wmc_sweeps_band_f32.                                     */
+/* ---------------------------------------------------------------------- */
+CF_API int cf_wmc_sweeps_band_peer_f32(const float* src, int32_t src_row0, int32_t src_rows,
+                                       float* dst, int32_t dst_row0, int32_t w, int32_t h,
+                                       int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,
+                                       float dt, int32_t iter_base, int32_t* d_flag,
+                                       float* peer_up, int32_t peer_up_row0, int32_t peer_up_end,
+                                       float* peer_dn, int32_t peer_dn_row0,
+                                       int32_t peer_dn_begin, void* stream);
+/* CUDA IPC / event plumbing for that protocol (handles are 64 bytes).       */
+CF_API int cf_device_alloc(size_t bytes, void** dptr);
+CF_API int cf_device_free(void* dptr);
+CF_API int cf_copy(void* dst, const void* src, size_t bytes, void* stream);
+CF_API int cf_ipc_mem_handle(const void* dptr, void* handle_out);
+CF_API int cf_ipc_open_mem(const void* handle, void** dptr);
+CF_API int cf_ipc_close_mem(void* dptr);
+CF_API int cf_ipc_event_create(void** event);
+CF_API int cf_ipc_event_handle(void* event, void* handle_out);
+CF_API int cf_ipc_open_event(const void* handle, void** event);
+CF_API int cf_event_record(void* event, void* stream);
+CF_API int cf_stream_wait_event(void* stream, void* event);
+CF_API int cf_event_destroy(void* event);
+CF_API int cf_stream_synchronize(void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* Row-band primitive for sharded filtering (BASELINE cfg 4).               */
 /* Runs `sweeps` (1 <= sweeps <= cf_wmc_max_sweeps_per_launch()) Jacobi     */
 /* sweeps of the flow in ONE launch, producing global rows [y0, y1) of the  */

@@ -46,6 +46,22 @@ SIGNATURES = {
                                            _f32, _f32, _f32, _i32, _vp, _sz, _pi32, _vp]),
     "cf_shard_plan_init": (C.c_int, [_i32, _i32, _i32, _i32, _vp]),
     "cf_wmc_filter_sharded_f32": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f32, _pi32]),
+    "cf_wmc_sweeps_band_peer_f32": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i32,
+                                              _i32, _i32, _f32, _i32, _vp, _vp, _i32, _i32, _vp,
+                                              _i32, _i32, _vp]),
+    "cf_device_alloc": (C.c_int, [_sz, C.POINTER(_vp)]),
+    "cf_device_free": (C.c_int, [_vp]),
+    "cf_copy": (C.c_int, [_vp, _vp, _sz, _vp]),
+    "cf_ipc_mem_handle": (C.c_int, [_vp, _vp]),
+    "cf_ipc_open_mem": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "cf_ipc_close_mem": (C.c_int, [_vp]),
+    "cf_ipc_event_create": (C.c_int, [C.POINTER(_vp)]),
+    "cf_ipc_event_handle": (C.c_int, [_vp, _vp]),
+    "cf_ipc_open_event": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "cf_event_record": (C.c_int, [_vp, _vp]),
+    "cf_stream_wait_event": (C.c_int, [_vp, _vp]),
+    "cf_event_destroy": (C.c_int, [_vp]),
+    "cf_stream_synchronize": (C.c_int, [_vp]),
     "cf_wmc_max_sweeps_per_launch": (_i32, []),
     "cf_wmc_filter_launches": (_i32, [_i32, _i32, _i32, _i32]),
     "cf_wmc_filter_sweeps_per_launch": (_i32, [_i32, _i32, _i32]),

@@ -473,6 +473,34 @@ CF_API int cf_wmc_filter_query_nonfinite(const void* workspace, int32_t* first_b
     return CF_ENONFINITE;
 }
 
+CF_API int cf_wmc_sweeps_band_peer_f32(const float* src, int32_t src_row0, int32_t src_rows,
+                                       float* dst, int32_t dst_row0, int32_t w, int32_t h,
+                                       int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,
+                                       float dt, int32_t iter_base, int32_t* d_flag,
+                                       float* peer_up, int32_t peer_up_row0, int32_t peer_up_end,
+                                       float* peer_dn, int32_t peer_dn_row0,
+                                       int32_t peer_dn_begin, void* stream) {
+    if (!src || !dst || w <= 0 || h <= 0 || pitch < w) return CF_EINVAL;
+    if (sweeps < 1 || sweeps > kMaxLevels || !(dt > 0.0f) || dt > 1.0f) return CF_EINVAL;
+    if (y0 < 0 || y1 > h || y0 >= y1) return CF_EINVAL;
+    const int need0 = std::max(0, y0 - sweeps), need1 = std::min(h, y1 + sweeps);
+    if (src_row0 > need0 || src_row0 + src_rows < need1) return CF_EINVAL;
+    if (peer_up && (peer_up_end < y0 || peer_up_end > y1 || peer_up_row0 > y0)) return CF_EINVAL;
+    if (peer_dn && (peer_dn_begin < y0 || peer_dn_begin > y1)) return CF_EINVAL;
+    DevInfo d;
+    if (int rc = device_info(&d)) return rc;
+    cfk::SweepParams p{};
+    p.src = src; p.dst = dst;
+    p.src_pitch = p.dst_pitch = pitch;
+    p.src_plane = p.dst_plane = 0;
+    p.src_row0 = src_row0; p.dst_row0 = dst_row0;
+    p.w = w; p.h = h; p.y0 = y0; p.y1 = y1; p.planes = 1;
+    p.dt = dt; p.iter_base = iter_base; p.flag = d_flag;
+    p.peer_up = peer_up; p.peer_up_row0 = peer_up_row0; p.peer_up_end = peer_up_end;
+    p.peer_dn = peer_dn; p.peer_dn_row0 = peer_dn_row0; p.peer_dn_begin = peer_dn_begin;
+    return launch<cfk::kModeFlow>(p, sweeps, d, (cudaStream_t)stream);
+}
+
 CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,
                                   float* dst, int32_t dst_row0, int32_t w, int32_t h,
                                   int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,

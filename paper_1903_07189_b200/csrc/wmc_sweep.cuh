@@ -103,6 +103,14 @@ struct SweepParams {
     float dt;
     int32_t iter_base;
     int32_t* flag;            // nullable
+    // Fused halo stores (row-band sharding): level-K rows
+    // y < peer_up_end are also written into peer_up -- the upper neighbour's
+    // destination buffer, whose row 0 is global row peer_up_row0 -- and rows
+    // y >= peer_dn_begin into peer_dn.  Both null: no peer stores.  Peer rows
+    // are always produced by checked steps, so the fast loop is unchanged.
+    float* peer_up;
+    float* peer_dn;
+    int32_t peer_up_row0, peer_up_end, peer_dn_row0, peer_dn_begin;
     // MODE == kModeL2 (solve_l2_area): data term f and lambda
     const float* fdata;       // global row 0 of plane 0 (same column geometry as src)
     int64_t f_pitch, f_plane; // elements
@@ -562,6 +570,16 @@ struct SweepWarp {
         if constexpr (L < K) store<L + 1, CHECKED, EDGE>(t, R4, sptr);
     }
 
+    // This lane's output columns of a level-K row (bounds-checked).
+    __device__ __forceinline__ void store_row(float* row, const f2 (&nv)[C]) const {
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            if (!outc[j]) continue;
+            if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = lo(nv[j]);
+            if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = hi(nv[j]);
+        }
+    }
+
     template <int L, bool CHECKED, bool EDGE = false>
     __device__ __forceinline__ void store_one(int t, const uint32_t (&R4)[4], float* sptr) {
         const int y = t - lag(L);
@@ -581,12 +599,11 @@ struct SweepWarp {
         if constexpr (L == K) {
             if (CHECKED || EDGE) {
                 float* row = dstp + (int64_t)(y - P.dst_row0) * P.dst_pitch;
-#pragma unroll
-                for (int j = 0; j < C; ++j) {
-                    if (!outc[j]) continue;
-                    if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = lo(nv[j]);
-                    if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = hi(nv[j]);
-                }
+                store_row(row, nv);
+                if (CHECKED && P.peer_up && y < P.peer_up_end)  // into the neighbour's halo
+                    store_row(P.peer_up + (int64_t)(y - P.peer_up_row0) * P.dst_pitch, nv);
+                if (CHECKED && P.peer_dn && y >= P.peer_dn_begin)
+                    store_row(P.peer_dn + (int64_t)(y - P.peer_dn_row0) * P.dst_pitch, nv);
             } else {  // sptr: row y at column xf[0]; chunk 1 is G::S columns on
 #pragma unroll
                 for (int j = 0; j < C; ++j) {
@@ -640,6 +657,8 @@ struct SweepWarp {
             t_s = max(t_s, max(rlo(L) + 1, 1) + lag(L));    // y-1 >= 0, y > rlo (carries)
             t_e = min(t_e, min(rhi(L) - 1, P.h - 2) + lag(L));  // y+1 <= h-1, y < rhi
         }
+        if (P.peer_up) t_s = max(t_s, P.peer_up_end + lag(K));       // peer rows: checked
+        if (P.peer_dn) t_e = min(t_e, P.peer_dn_begin - 1 + lag(K));
 #pragma unroll
         for (int L = 0; L <= K; ++L)
 #pragma unroll

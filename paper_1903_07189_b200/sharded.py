@@ -247,3 +247,169 @@ def filter_sharded(img, iters: int, dt: float = 1.0, parts: int = 2, devices=Non
         out[pl.row0[p]:pl.row1[p]] = band.to(out.device)
     return out.cpu().numpy() if host else out
 
+
+
+class IpcBandFlow:
+    """Row-band flow across processes with the halo exchange FUSED into the
+    band kernel: each rank's launch stores the boundary rows
+    its neighbours need next straight into their buffers (CUDA IPC peer
+    memory; NVLink between GPUs) via cf_wmc_sweeps_band_peer_f32.  No
+    collective runs per launch: ordering is interprocess CUDA events plus a
+    launch counter per rank in POSIX shared memory (a rank waits on a
+    neighbour's event only after the counter shows it was recorded), and
+    `dist` is used once, to exchange the IPC handles.  No kernel waits on
+    another, so ranks may share one GPU (the tests do).
+
+    Launch i of rank p reads bufs[i % 2] (its band + halos) and writes
+    bufs[(i+1) % 2]; it waits first for both neighbours' launch i-1 (they
+    wrote its halos, and it is about to overwrite theirs in the buffer their
+    launch i-1 read)."""
+
+    RING = 4  # events per rank; neighbours lag by at most 2 launches
+
+    def __init__(self, layout: BandLayout, dist, shm_name: str, group=None):
+        import ctypes as C
+
+        import numpy as np
+        from multiprocessing import shared_memory
+
+        from ._lib import check, lib
+        self.L, self.C, self.np = layout, C, np
+        L, self._lib = layout, lib()
+        self._check = check
+        self.w = L.w
+        self.row_bytes = L.w * 4
+        self.bufs, self.events = [], []
+        for _ in range(2):
+            p = C.c_void_p()
+            check(self._lib.cf_device_alloc(L.rows * self.row_bytes, C.byref(p)), "alloc")
+            self.bufs.append(p.value)
+        flag = C.c_void_p()
+        check(self._lib.cf_device_alloc(256, C.byref(flag)), "alloc flag")
+        self.flag = flag.value
+        for _ in range(self.RING):
+            e = C.c_void_p()
+            check(self._lib.cf_ipc_event_create(C.byref(e)), "ipc event")
+            self.events.append(e.value)
+
+        def handle(fn, obj):
+            buf = C.create_string_buffer(64)
+            check(fn(obj, buf), "ipc handle")
+            return buf.raw
+        mine = {"rank": L.rank, "r0": L.r0, "r1": L.r1, "buf_row0": L.buf_row0,
+                "mem": [handle(self._lib.cf_ipc_mem_handle, b) for b in self.bufs],
+                "ev": [handle(self._lib.cf_ipc_event_handle, e) for e in self.events]}
+        everyone = [None] * L.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.nbr = {}
+        for side, q in (("up", L.rank - 1), ("dn", L.rank + 1)):
+            if 0 <= q < L.world:
+                o = everyone[q]
+                mem = []
+                for hb in o["mem"]:
+                    p = C.c_void_p()
+                    check(self._lib.cf_ipc_open_mem(hb, C.byref(p)), "ipc open mem")
+                    mem.append(p.value)
+                ev = []
+                for hb in o["ev"]:
+                    e = C.c_void_p()
+                    check(self._lib.cf_ipc_open_event(hb, C.byref(e)), "ipc open event")
+                    ev.append(e.value)
+                self.nbr[side] = {"rank": q, "buf_row0": o["buf_row0"], "mem": mem, "ev": ev}
+        if L.rank == 0:
+            self.shm = shared_memory.SharedMemory(name=shm_name, create=True, size=8 * L.world)
+        dist.barrier(group=group)
+        if L.rank != 0:
+            self.shm = shared_memory.SharedMemory(name=shm_name)
+        self.count = np.ndarray((L.world,), dtype=np.int64, buffer=self.shm.buf)
+        self.count[L.rank] = -1
+        dist.barrier(group=group)
+        self.dist, self.group = dist, group
+
+    def _row_ptr(self, base: int, buf_row0: int, y: int) -> int:
+        return base + (y - buf_row0) * self.row_bytes
+
+    def load(self, band) -> None:
+        """Place the owned rows (host float32, (r1 - r0) x w) into bufs[0]."""
+        arr = self.np.ascontiguousarray(band, dtype=self.np.float32)
+        L = self.L
+        self._check(self._lib.cf_copy(self._row_ptr(self.bufs[0], L.buf_row0, L.r0),
+                                      arr.ctypes.data, arr.nbytes, None), "load")
+        self._check(self._lib.cf_stream_synchronize(None), "sync")
+
+    def _wait(self, i: int, stream) -> None:
+        import time
+        for side in ("up", "dn"):
+            if side in self.nbr:
+                q = self.nbr[side]
+                while self.count[q["rank"]] < i:
+                    time.sleep(0)
+                self._check(self._lib.cf_stream_wait_event(stream, q["ev"][i % self.RING]),
+                            "wait event")
+
+    def _publish(self, i: int, stream) -> None:
+        self._check(self._lib.cf_event_record(self.events[i % self.RING], stream), "record")
+        self.count[self.L.rank] = i
+
+    def run(self, iters: int, dt: float, stream=None) -> int:
+        """Advance iters Jacobi sweeps; returns the index of the result buffer."""
+        L, lib = self.L, self._lib
+        sched = launch_schedule(iters, L.k)
+        if not sched:
+            return 0
+        kk0 = sched[0]
+        # initial halo fill: our boundary rows into the neighbours' bufs[0]
+        for side, rows in (("up", (L.r0, L.r0 + kk0)), ("dn", (L.r1 - kk0, L.r1))):
+            if side in self.nbr:
+                q = self.nbr[side]
+                self._check(lib.cf_copy(self._row_ptr(q["mem"][0], q["buf_row0"], rows[0]),
+                                        self._row_ptr(self.bufs[0], L.buf_row0, rows[0]),
+                                        (rows[1] - rows[0]) * self.row_bytes, stream), "halo")
+        self._publish(0, stream)
+        it = 0
+        for i, kk in enumerate(sched):
+            self._wait(i, stream)
+            nk = sched[i + 1] if i + 1 < len(sched) else 0
+            src, dst = self.bufs[i % 2], self.bufs[(i + 1) % 2]
+            up, dn = self.nbr.get("up"), self.nbr.get("dn")
+            rc = lib.cf_wmc_sweeps_band_peer_f32(
+                src, L.buf_row0, L.rows, dst, L.buf_row0, L.w, L.h, L.w, L.r0, L.r1, kk,
+                float(dt), it, self.flag,
+                up["mem"][(i + 1) % 2] if up and nk else None,
+                up["buf_row0"] if up else 0, L.r0 + nk,
+                dn["mem"][(i + 1) % 2] if dn and nk else None,
+                dn["buf_row0"] if dn else 0, L.r1 - nk, stream)
+            self._check(rc, "band launch")
+            self._publish(i + 1, stream)
+            it += kk
+        return len(sched) % 2
+
+    def read(self, which: int):
+        """The owned rows of bufs[which] (host float32)."""
+        L = self.L
+        out = self.np.empty((L.r1 - L.r0, L.w), dtype=self.np.float32)
+        self._check(self._lib.cf_stream_synchronize(None), "sync")
+        self._check(self._lib.cf_copy(out.ctypes.data,
+                                      self._row_ptr(self.bufs[which], L.buf_row0, L.r0),
+                                      out.nbytes, None), "read")
+        self._check(self._lib.cf_stream_synchronize(None), "sync")
+        return out
+
+    def close(self) -> None:
+        """Collective: every rank must call it (neighbours stop writing first)."""
+        self._check(self._lib.cf_stream_synchronize(None), "sync")
+        self.dist.barrier(group=self.group)
+        for q in self.nbr.values():
+            for p in q["mem"]:
+                self._lib.cf_ipc_close_mem(p)
+            for e in q["ev"]:
+                self._lib.cf_event_destroy(e)
+        for e in self.events:
+            self._lib.cf_event_destroy(e)
+        for b in self.bufs:
+            self._lib.cf_device_free(b)
+        self._lib.cf_device_free(self.flag)
+        self.shm.close()
+        self.dist.barrier(group=self.group)
+        if self.L.rank == 0:
+            self.shm.unlink()
