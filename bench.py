@@ -182,10 +182,19 @@ def bench_b200(args, cfg):
     from paper_1903_07189_b200 import sharded
 
     world, rank, local = dist_env()
+    # CF_BENCH_DEVICE (testing only): put every rank on one device, to run the
+    # N > 1 code path on a single GPU (timings then mean nothing)
+    local = int(os.environ.get("CF_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # the IPC halo path needs no collective on the device: gloo for the few
+    # host barriers / reductions (and NCCL rejects two ranks on one device)
+    backend = "gloo" if args.halo == "ipc" else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     L = cf.lib()
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
@@ -232,6 +241,17 @@ def bench_b200(args, cfg):
             rc = L.cf_wmc_map_f32(dev_in.data_ptr(), out.data_ptr(), W, H, W, P, H * W, cur_sp())
             assert rc == 0, rc
         launches_per_step = 1
+    elif world > 1 and cfg.sharding == "rows" and args.halo == "ipc":
+        # halo exchange fused into the band kernel (CUDA IPC peer stores)
+        flow = sharded.IpcBandFlow(lay, dist, f"cf_bench_{os.environ.get('MASTER_PORT', '0')}")
+        band_ptr = flow._row_ptr(flow.bufs[0], lay.buf_row0, lay.r0)
+        band_bytes = dev_in.numel() * 4
+        ipc_result = [0]
+
+        def step():
+            assert L.cf_copy(band_ptr, dev_in.data_ptr(), band_bytes, sp) == 0
+            ipc_result[0] = flow.run(cfg.iters, cfg.dt, stream=sp)
+        launches_per_step = len(sharded.launch_schedule(cfg.iters, K))
     elif world > 1 and cfg.sharding == "rows":
         buf_a = torch.zeros((lay.rows, cfg.w), dtype=torch.float32, device=dev)
         buf_b = torch.zeros_like(buf_a)
@@ -295,7 +315,7 @@ def bench_b200(args, cfg):
         barrier()
         ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms / steps
@@ -375,6 +395,28 @@ def bench_b200(args, cfg):
         torch.cuda.synchronize(dev)
         kern_ms = e0.elapsed_time(e1) / (2 * reps)
         kern_updates = n_px_local * K
+    elif cfg.iters > 0 and cfg.sharding == "rows":
+        # row bands: the K-sweep band kernel on this rank's own band
+        if args.halo == "ipc":
+            src_p, dst_p = flow.bufs[0], flow.bufs[1]
+        else:
+            src_p, dst_p = buf_a.data_ptr(), buf_b.data_ptr()
+        reps = 10
+
+        def band_launch(a, b):
+            rc = L.cf_wmc_sweeps_band_f32(a, lay.buf_row0, lay.rows, b, lay.buf_row0, cfg.w, cfg.h,
+                                          cfg.w, lay.r0, lay.r1, K, cfg.dt, 0, None, sp)
+            assert rc == 0, rc
+        band_launch(src_p, dst_p)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for i in range(reps):
+            band_launch(src_p if i % 2 == 0 else dst_p, dst_p if i % 2 == 0 else src_p)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        kern_ms = e0.elapsed_time(e1) / reps
+        kern_updates = (lay.r1 - lay.r0) * cfg.w * K
     elif cfg.iters == 0:
         kern_ms, kern_updates = ms_step, n_px_local
     peak, peak_src = peaks()
@@ -429,6 +471,12 @@ def bench_b200(args, cfg):
                 s_out.wait_event(ev_c)
                 out_host.copy_(res.reshape(out_host.shape), non_blocking=True)
                 ev_out[b].record(s_out)
+    elif args.halo == "ipc":
+        def e2e_step():
+            assert L.cf_copy(band_ptr, host_t.data_ptr(), band_bytes, sp) == 0
+            which = flow.run(cfg.iters, cfg.dt, stream=sp)
+            src = flow._row_ptr(flow.bufs[which], lay.buf_row0, lay.r0)
+            assert L.cf_copy(out_host.data_ptr(), src, band_bytes, sp) == 0
     else:
         def e2e_step():
             d_in = host_t.to(dev, non_blocking=True)
@@ -449,7 +497,7 @@ def bench_b200(args, cfg):
         barrier()
         ms = t0.elapsed_time(t1)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms / steps
@@ -469,6 +517,8 @@ def bench_b200(args, cfg):
     h2d = host_t.numel() * host_t.element_size()
     d2h = out_host.numel() * out_host.element_size()
 
+    if world > 1 and cfg.sharding == "rows" and args.halo == "ipc":
+        flow.close()  # collective: neighbours stop writing before unmapping
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -485,7 +535,7 @@ def bench_b200(args, cfg):
             "workload": workload_name(cfg),
             "iters": cfg.iters, "planes": cfg.planes, "h": cfg.h, "w": cfg.w,
             "sweeps_per_launch": 1 if cfg.iters == 0 else K,
-            "parallelism": (f"rowband{world}" if cfg.sharding == "rows" and world > 1 else
+            "parallelism": (f"rowband{world}-{args.halo}" if cfg.sharding == "rows" and world > 1 else
                             f"images{world}" if world > 1 else "single"),
             "l2": ("inputs larger than L2 (126 MB)" if not l2_resident else
                    "working set fits in L2: 256 MiB flush between timed steps"),
@@ -587,6 +637,10 @@ def main():
     ap.add_argument("--all", default=None, help="run every config (+ the supplemental 16384^2 "
                     "map) at N=1, write JSON lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "ipc"],
+                    help="row-band halo exchange at N > 1: NCCL send/recv overlapped with the "
+                         "band interior (default) or fused into the band kernel's stores over "
+                         "CUDA IPC peer memory")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     from paper_1903_07189_b200.configs import CONFIGS, SUPPLEMENTAL

@@ -265,7 +265,7 @@ class IpcBandFlow:
     wrote its halos, and it is about to overwrite theirs in the buffer their
     launch i-1 read)."""
 
-    RING = 4  # events per rank; neighbours lag by at most 2 launches
+    RING = 4  # events per rank; neighbours lag by at most 2 sequence numbers
 
     def __init__(self, layout: BandLayout, dist, shm_name: str, group=None):
         import ctypes as C
@@ -325,6 +325,7 @@ class IpcBandFlow:
         self.count[L.rank] = -1
         dist.barrier(group=group)
         self.dist, self.group = dist, group
+        self.seq = 0  # launches are numbered across runs (counters only grow)
 
     def _row_ptr(self, base: int, buf_row0: int, y: int) -> int:
         return base + (y - buf_row0) * self.row_bytes
@@ -352,11 +353,17 @@ class IpcBandFlow:
         self.count[self.L.rank] = i
 
     def run(self, iters: int, dt: float, stream=None) -> int:
-        """Advance iters Jacobi sweeps; returns the index of the result buffer."""
+        """Advance iters Jacobi sweeps from bufs[0]; returns the index of the
+        result buffer.  Runs may follow each other without a barrier: each
+        run first waits for the neighbours' last launch of the previous one
+        (their halo reads end before this run's initial fill overwrites them)."""
         L, lib = self.L, self._lib
         sched = launch_schedule(iters, L.k)
         if not sched:
             return 0
+        base = self.seq
+        if base > 0:
+            self._wait(base, stream)
         kk0 = sched[0]
         # initial halo fill: our boundary rows into the neighbours' bufs[0]
         for side, rows in (("up", (L.r0, L.r0 + kk0)), ("dn", (L.r1 - kk0, L.r1))):
@@ -365,10 +372,10 @@ class IpcBandFlow:
                 self._check(lib.cf_copy(self._row_ptr(q["mem"][0], q["buf_row0"], rows[0]),
                                         self._row_ptr(self.bufs[0], L.buf_row0, rows[0]),
                                         (rows[1] - rows[0]) * self.row_bytes, stream), "halo")
-        self._publish(0, stream)
+        self._publish(base + 1, stream)
         it = 0
         for i, kk in enumerate(sched):
-            self._wait(i, stream)
+            self._wait(base + 1 + i, stream)
             nk = sched[i + 1] if i + 1 < len(sched) else 0
             src, dst = self.bufs[i % 2], self.bufs[(i + 1) % 2]
             up, dn = self.nbr.get("up"), self.nbr.get("dn")
@@ -380,8 +387,9 @@ class IpcBandFlow:
                 dn["mem"][(i + 1) % 2] if dn and nk else None,
                 dn["buf_row0"] if dn else 0, L.r1 - nk, stream)
             self._check(rc, "band launch")
-            self._publish(i + 1, stream)
+            self._publish(base + 2 + i, stream)
             it += kk
+        self.seq = base + 1 + len(sched)
         return len(sched) % 2
 
     def read(self, which: int):
