@@ -187,9 +187,9 @@ def bench_b200(args, cfg):
     local = int(os.environ.get("CF_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # the IPC halo path needs no collective on the device: gloo for the few
-    # host barriers / reductions (and NCCL rejects two ranks on one device)
-    backend = "gloo" if args.halo == "ipc" else "nccl"
+    # ranks sharing a device (CF_BENCH_DEVICE, IPC halo only -- it needs no
+    # device collective) use gloo for the few host barriers; NCCL otherwise
+    backend = "gloo" if args.halo == "ipc" and "CF_BENCH_DEVICE" in os.environ else "nccl"
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
