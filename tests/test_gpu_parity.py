@@ -611,3 +611,24 @@ def test_concurrent_streams():
     torch.cuda.synchronize()
     for o, r in zip(outs, refs):
         assert_bitexact(o.cpu().numpy(), r, "concurrent stream")
+
+
+def test_linear_scaling_in_pixels():
+    """SPEC acceptance 13 on the GPU: 4x the pixels takes 3.2-5.0x the time
+    (filter, 20 iterations, 4096^2 vs 8192^2; best of 5, CUDA events)."""
+    def best_ms(n):
+        x = torch.rand((n, n), device="cuda")
+        ws = torch.empty(cf.workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+        cfg = cf.FlowConfig(iters=20)
+        cf.mc_flow(x, cfg, workspace=ws, inplace=True, check_finite=False)
+        times = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            cf.mc_flow(x, cfg, workspace=ws, inplace=True, check_finite=False)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        return min(times)
+    ratio = best_ms(8192) / best_ms(4096)
+    assert 3.2 <= ratio <= 5.0, ratio
