@@ -632,3 +632,16 @@ def test_linear_scaling_in_pixels():
         return min(times)
     ratio = best_ms(8192) / best_ms(4096)
     assert 3.2 <= ratio <= 5.0, ratio
+
+
+@pytest.mark.parametrize("P,h,w", [(1, 700, 777), (2, 600, 513), (1, 3001, 177), (1, 521, 1031),
+                                   (3, 257, 700)])
+def test_streaming_map_odd_shapes(P, h, w):
+    """Maps above the flat-kernel threshold (> 512 Ki pixels) take the
+    streaming map kernel: odd widths / heights, planes, ties (quantised
+    values), bit-exact vs the oracle."""
+    rng = np.random.default_rng(h * w)
+    img = (np.round(rng.random((P, h, w)) * 8) / 8).astype(np.float32)
+    img += (rng.random((P, h, w)) * 1e-3).astype(np.float32) * (rng.random((P, h, w)) < 0.5)
+    got = cf.wmc_half_laplace(torch.from_numpy(img).cuda()).cpu().numpy()
+    assert_bitexact(got, oracle.wmc_map_f32(img), f"map {P}x{h}x{w}")
