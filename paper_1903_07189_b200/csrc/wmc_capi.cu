@@ -34,6 +34,11 @@ constexpr int kFlowLevels = CF_FLOW_LEVELS;
 #define CF_FLAT_MAP_PIXELS (1 << 19)  // measured crossover: +23 % at 512^2, equal at 1024^2
 #endif
 constexpr int64_t kFlatMapPixels = CF_FLAT_MAP_PIXELS;  // maps up to this size: flat kernel
+#ifndef CF_BORDER_SPLIT
+#define CF_BORDER_SPLIT 2
+#endif
+constexpr int kBorderSplit = CF_BORDER_SPLIT;  // border-pair strips are this much shorter
+constexpr int kBorderSplitMinRows = 32;         // ... when interior strips are this long
 constexpr size_t kWsHeader = 256;        // workspace: [flag | pad] then image
 constexpr int32_t kFlagNone = 0x7f7f7f7f;  // memset(0x7f) pattern
 
@@ -103,9 +108,17 @@ int kernel_occupancy_warps() {
 
 // Strip planner: choose rows per warp-task so that the number of waves times
 // the per-task length (rows + temporal warm-up + fixed cost) is minimal.
+// Border pairs' strip height: kBorderSplit x shorter for long strips (there
+// they were the launch's tail); short strips (latency-bound small images)
+// keep the interior height -- extra warps cost more than the tail there.
+int border_strip_rows(int sr) {
+    return sr >= kBorderSplitMinRows ? (sr + kBorderSplit - 1) / kBorderSplit : sr;
+}
+
 void plan_strips(cfk::SweepParams& p, int K, int slots) {
     const int rows = p.y1 - p.y0;
-    const int64_t per_strip_tasks = (int64_t)((p.n_chunks + 1) / 2) * p.planes;
+    const int64_t n_pairs = (p.n_chunks + 1) / 2;
+    const int64_t nb = std::min<int64_t>(n_pairs, 1 + p.n_bhi), ni = n_pairs - nb;
 #ifndef CF_PLAN_OVH
 #define CF_PLAN_OVH 6.0
 #endif
@@ -116,7 +129,10 @@ void plan_strips(cfk::SweepParams& p, int K, int slots) {
     for (int ns = 1; ns <= max_strips; ++ns) {
         const int sr = (rows + ns - 1) / ns;
         const int ns_eff = (rows + sr - 1) / sr;
-        const int64_t tasks = per_strip_tasks * ns_eff;
+        const int sr_b = border_strip_rows(sr);
+        const int ns_b = (rows + sr_b - 1) / sr_b;
+        // all tasks, border ones included (kBorderSplit x more, shorter)
+        const int64_t tasks = (ni * ns_eff + nb * ns_b) * p.planes;
         const int64_t waves = (tasks + slots - 1) / slots;
         const double cost = (double)waves * (sr + overhead);
         if (cost < best_cost * 0.999) { best_cost = cost; best = ns; }
@@ -124,6 +140,8 @@ void plan_strips(cfk::SweepParams& p, int K, int slots) {
     }
     p.strip_rows = (rows + best - 1) / best;
     p.n_strips = (rows + p.strip_rows - 1) / p.strip_rows;
+    p.strip_rows_b = border_strip_rows(p.strip_rows);
+    p.n_strips_b = (rows + p.strip_rows_b - 1) / p.strip_rows_b;
 }
 
 template <int K, int MODE>
@@ -145,7 +163,9 @@ int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
         p.n_bhi = nbh;
     }
     plan_strips(p, K, d.sms * kernel_occupancy_warps<K, MODE>());
-    const int64_t tasks = (int64_t)((p.n_chunks + 1) / 2) * p.n_strips * p.planes;
+    const int64_t n_pairs = (p.n_chunks + 1) / 2;
+    const int64_t nb = std::min<int64_t>(n_pairs, 1 + p.n_bhi);
+    const int64_t tasks = (nb * p.n_strips_b + (n_pairs - nb) * p.n_strips) * p.planes;
     const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
     if (blocks > INT_MAX) return CF_EINVAL;
     cfk::wmc_sweeps_kernel<K, MODE><<<(unsigned)blocks, cfk::kThreads, smem_bytes<K>(), s>>>(p);

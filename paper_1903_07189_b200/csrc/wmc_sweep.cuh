@@ -100,6 +100,7 @@ struct SweepParams {
     int32_t y0, y1;           // output rows
     int32_t strip_rows, n_strips, n_chunks, planes;
     int32_t n_bhi;            // trailing border chunk pairs (host, launch_k)
+    int32_t strip_rows_b, n_strips_b;  // border pairs' (shorter) strips
     float dt;
     int32_t iter_base;
     int32_t* flag;            // nullable
@@ -780,27 +781,31 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     const int n_pairs = (p.n_chunks + 1) / 2;
-    const int total = n_pairs * p.n_strips * p.planes;
+    const int nb = min(n_pairs, 1 + p.n_bhi), ni = n_pairs - nb;
+    const int btasks = nb * p.n_strips_b * p.planes;
+    const int total = btasks + ni * p.n_strips * p.planes;
     if (warp >= total) return;  // warp-uniform
     // Border chunk pairs (pair 0 and the last n_bhi) do extra per-step work
     // (edge fix, clamped prefetch): their tasks take the lowest warp indices,
     // so they start first and share blocks with each other rather than
     // stretching the residency of otherwise-fast blocks (a block frees its
     // slot only when its slowest warp ends).
-    const int nb = min(n_pairs, 1 + p.n_bhi);
-    const int btasks = nb * p.n_strips * p.planes;
-    int cpair, rest;
+    // Border pairs also get shorter strips (strip_rows_b): their steps cost
+    // more, and with equal strips they were the tail of every launch.
+    int cpair, strip, plane, srows;
     if (warp < btasks) {
-        const int k = warp % nb;
-        rest = warp / nb;
+        const int k = warp % nb, rest = warp / nb;
         cpair = k == 0 ? 0 : n_pairs - nb + k;
+        strip = rest % p.n_strips_b;
+        plane = rest / p.n_strips_b;
+        srows = p.strip_rows_b;
     } else {
-        const int i = warp - btasks, ni = n_pairs - nb;
+        const int i = warp - btasks, rest = i / ni;
         cpair = 1 + i % ni;
-        rest = i / ni;
+        strip = rest % p.n_strips;
+        plane = rest / p.n_strips;
+        srows = p.strip_rows;
     }
-    const int strip = rest % p.n_strips;
-    const int plane = rest / p.n_strips;
 
     SweepWarp<K, MODE> sw(p);
     sw.lane = threadIdx.x & 31;
@@ -828,9 +833,12 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
             if (x == 0) sw.emask |= 1u << (4 * j + 2 * h);
             if (x == p.w - 1) sw.emask |= 1u << (4 * j + 2 * h + 1);
         }
-    sw.ys = p.y0 + strip * p.strip_rows;
-    sw.ye = min(sw.ys + p.strip_rows, p.y1);
+    sw.ys = p.y0 + strip * srows;
+    sw.ye = min(sw.ys + srows, p.y1);
     if (sw.ys >= sw.ye) return;
+#ifdef CF_EXP_SKIP_BORDER  // diagnostic only (wrong results): cost of the border tasks
+    if (sw.border) return;
+#endif
     sw.srcp = p.src + (int64_t)plane * p.src_plane;
     sw.dstp = p.dst + (int64_t)plane * p.dst_plane;
     sw.fp = (MODE == kModeL2 || MODE == kModeL1) ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
