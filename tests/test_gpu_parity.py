@@ -645,3 +645,24 @@ def test_streaming_map_odd_shapes(P, h, w):
     img += (rng.random((P, h, w)) * 1e-3).astype(np.float32) * (rng.random((P, h, w)) < 0.5)
     got = cf.wmc_half_laplace(torch.from_numpy(img).cuda()).cpu().numpy()
     assert_bitexact(got, oracle.wmc_map_f32(img), f"map {P}x{h}x{w}")
+
+
+def test_fuzz_large_geometries():
+    """Seeded random LARGE shapes (long strips, multi-wave grids, split
+    border strips): filter and map bit-exact vs the oracle."""
+    rng = np.random.default_rng(424242)
+    for case in range(6):
+        h, w = int(rng.integers(600, 3000)), int(rng.integers(600, 6000))
+        P = int(rng.integers(1, 3))
+        iters = int(rng.integers(2, 9))
+        dt = float(np.float32(rng.uniform(0.2, 1.0)))
+        g = torch.Generator(device="cuda").manual_seed(case)
+        x = torch.rand((P, h, w), device="cuda", generator=g)
+        src = x.cpu().numpy()
+        if case == 0:
+            assert_bitexact(cf.wmc_half_laplace(x).cpu().numpy(), oracle.wmc_map_f32(src),
+                            f"large map {P}x{h}x{w}")
+        out = cf.mc_flow(x, cf.FlowConfig(dt=dt, iters=iters)).cpu().numpy()
+        ref, bad = oracle.flow_f32(src, iters, dt)
+        assert bad == 0
+        assert_bitexact(out, ref, f"large fuzz {P}x{h}x{w} it {iters} dt {dt}")
