@@ -203,6 +203,78 @@ inline SolveReport solve_l1_area(const Image2D& f, SolverConfig cfg, cudaStream_
     return solve(f, cfg, s);
 }
 
+// mc_flow of one image split into `parts` row bands over `devices` (the
+// reference's for_rows chunking; cf_wmc_filter_sharded_f32): host in / host
+// out.  devices.empty(): every part on the current device.
+inline Image2D mc_flow_sharded(const Image2D& img, const FlowConfig& cfg, int parts,
+                               std::vector<int> devices = {}) {
+    if (cfg.iters == 0) return img;
+    const int w = img.width, h = img.height;
+    int cur = 0;
+    detail::cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (devices.empty()) devices.assign(parts, cur);
+    if ((int)devices.size() != parts) throw std::invalid_argument("one device per part");
+    cf_shard_plan plan;
+    detail::check(cf_shard_plan_init(h, w, parts, cf_wmc_filter_sweeps_per_launch(w, h, 1), &plan),
+                  "cf_shard_plan_init");
+    struct Part {
+        int dev;
+        void *a = nullptr, *b = nullptr, *flag = nullptr;
+    };
+    std::vector<Part> ps(parts);
+    std::vector<float*> va(parts), vb(parts);
+    std::vector<int32_t*> vf(parts);
+    auto release = [&]() {
+        for (auto& p : ps) {
+            cudaSetDevice(p.dev);
+            cudaFree(p.a);
+            cudaFree(p.b);
+            cudaFree(p.flag);
+        }
+        cudaSetDevice(cur);
+    };
+    try {
+        for (int p = 0; p < parts; ++p) {
+            ps[p].dev = devices[p];
+            detail::cuda_check(cudaSetDevice(devices[p]), "cudaSetDevice");
+            const size_t bytes = (size_t)plan.rows[p] * w * sizeof(float);
+            detail::cuda_check(cudaMalloc(&ps[p].a, bytes), "cudaMalloc");
+            detail::cuda_check(cudaMalloc(&ps[p].b, bytes), "cudaMalloc");
+            detail::cuda_check(cudaMalloc(&ps[p].flag, 256), "cudaMalloc");
+            const size_t own = (size_t)(plan.row1[p] - plan.row0[p]) * w;
+            detail::cuda_check(
+                cudaMemcpy((float*)ps[p].a + (size_t)plan.top[p] * w,
+                           img.data.data() + (size_t)plan.row0[p] * w, own * sizeof(float),
+                           cudaMemcpyHostToDevice),
+                "H2D");
+            va[p] = (float*)ps[p].a;
+            vb[p] = (float*)ps[p].b;
+            vf[p] = (int32_t*)ps[p].flag;
+        }
+        detail::cuda_check(cudaSetDevice(cur), "cudaSetDevice");
+        int32_t bad = 0;
+        const int st = cf_wmc_filter_sharded_f32(&plan, va.data(), vb.data(), vf.data(),
+                                                 devices.data(), nullptr, cfg.iters,
+                                                 (float)cfg.dt, &bad);
+        if (st == CF_ENONFINITE) throw FlowError(bad);
+        detail::check(st, "mc_flow_sharded");
+        Image2D out(w, h);
+        for (int p = 0; p < parts; ++p) {
+            detail::cuda_check(cudaSetDevice(devices[p]), "cudaSetDevice");
+            const size_t own = (size_t)(plan.row1[p] - plan.row0[p]) * w;
+            detail::cuda_check(cudaMemcpy(out.data.data() + (size_t)plan.row0[p] * w,
+                                          va[p] + (size_t)plan.top[p] * w, own * sizeof(float),
+                                          cudaMemcpyDeviceToHost),
+                               "D2H");
+        }
+        release();
+        return out;
+    } catch (...) {
+        release();
+        throw;
+    }
+}
+
 // Per-channel processing: planes are independent.
 inline std::vector<Image2D> mc_flow(const std::vector<Image2D>& channels, const FlowConfig& cfg) {
     if (channels.size() != 1 && channels.size() != 3)

@@ -6,7 +6,9 @@
 // (PGM/PNG file I/O is out of scope):
 //
 //   curveflow_b200 op    --size H W --seed S           -> checksum of the map
-//   curveflow_b200 flow  --size H W --iters N --dt D   -> checksum of U^N
+//   curveflow_b200 flow  --size H W --iters N --dt D [--parts P]
+//                                                       -> checksum of U^N (P row bands:
+//                                                          the single-process sharded filter)
 //   curveflow_b200 bench --size H W --iters N --reps R -> Gpixel-updates/s
 //   curveflow_b200 smooth --model l1|l2 --lambda L --alpha A --iters N --dt D
 //                                                       -> checksum of U
@@ -46,6 +48,7 @@ int main(int argc, char** argv) {
     int H = 512, W = 512, iters = 100, reps = 3;
     uint64_t seed = 1;
     double dt = 1.0, lambda = 0.0, alpha = 1.0;
+    int parts = 1;
     bool dt_set = false;
     std::string model = "l2";
     for (int i = 2; i < argc; ++i) {
@@ -59,6 +62,8 @@ int main(int argc, char** argv) {
         } else if (!std::strcmp(argv[i], "--dt") && i + 1 < argc) {
             dt = std::atof(argv[++i]);
             dt_set = true;
+        } else if (!std::strcmp(argv[i], "--parts") && i + 1 < argc) {
+            parts = std::atoi(argv[++i]);
         } else if (!std::strcmp(argv[i], "--model") && i + 1 < argc) {
             model = argv[++i];
         } else if (!std::strcmp(argv[i], "--lambda") && i + 1 < argc) {
@@ -77,7 +82,8 @@ int main(int argc, char** argv) {
             std::printf("{\"op\": \"wmc\", \"h\": %d, \"w\": %d, \"fnv1a\": \"%016llx\"}\n", H, W,
                         (unsigned long long)fnv1a(m.data));
         } else if (cmd == "flow") {
-            auto u = curveflow::cuda::mc_flow(img, {dt, iters});
+            auto u = parts > 1 ? curveflow::cuda::mc_flow_sharded(img, {dt, iters}, parts)
+                               : curveflow::cuda::mc_flow(img, {dt, iters});
             std::printf("{\"op\": \"flow\", \"h\": %d, \"w\": %d, \"iters\": %d, \"fnv1a\": "
                         "\"%016llx\"}\n", H, W, iters, (unsigned long long)fnv1a(u.data));
         } else if (cmd == "smooth") {

@@ -153,6 +153,12 @@ def test_cpp_cli_matches_oracle():
     out = json.loads(subprocess.run([exe, "op", "--size", str(H), str(W), "--seed", "3"],
                                     capture_output=True, text=True, check=True).stdout)
     assert out["fnv1a"] == fnv(oracle.wmc_map_f32(img))
+    # flow split into row bands (curveflow::cuda::mc_flow_sharded, C++)
+    for parts in (2, 3):
+        out = json.loads(subprocess.run([exe, "flow", "--size", str(H), str(W), "--seed", "3",
+                                         "--iters", str(it), "--parts", str(parts)],
+                                        capture_output=True, text=True, check=True).stdout)
+        assert out["fnv1a"] == fnv(ref), parts
     # smooth through curveflow::cuda::solve
     for model in ("l1", "l2"):
         out = json.loads(subprocess.run(
