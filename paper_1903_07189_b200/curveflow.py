@@ -183,37 +183,31 @@ def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=
         raise TypeError("mc_flow_u8 expects uint8 input")
     s3, squeeze = _as_planes(src)
     P, H, W = s3.shape
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     if out_dtype == "u8":
         if out is None:
             out = torch.empty((P, H, W), dtype=torch.uint8, device=s3.device)
         nbytes = int(lib().cf_wmc_filter_u8_u8_workspace_bytes(W, H, P))
-        if workspace is None or workspace.numel() < nbytes:
-            workspace = torch.empty(nbytes, dtype=torch.uint8, device=s3.device)
-        bad = C.c_int32(0)
-        with torch.cuda.device(s3.device):
-            rc = lib().cf_wmc_filter_u8_u8(
-                s3.data_ptr(), W, H * W, out.data_ptr(), W, H * W, W, H, P, int(cfg.iters),
-                float(cfg.dt), workspace.data_ptr(), nbytes,
-                C.byref(bad) if check_finite else None, _stream_ptr(torch, s3.device))
-        if rc == CF_ENONFINITE:
-            raise FlowError(bad.value)
-        check(rc, "mc_flow_u8")
-        res = out[0] if squeeze else out
-        if host:
-            return res.cpu().numpy() if isinstance(img_u8, np.ndarray) else res.cpu()
-        return res
-    if out is None:
-        out = torch.empty((P, H, W), dtype=torch.float32, device=s3.device)
-    nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
-    if cfg.iters > 0 and (workspace is None or workspace.numel() < nbytes):
+        need_ws = True
+    else:
+        if out is None:
+            out = torch.empty((P, H, W), dtype=torch.float32, device=s3.device)
+        nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+        need_ws = cfg.iters > 0
+    if need_ws and (workspace is None or workspace.numel() < nbytes):
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=s3.device)
     bad = C.c_int32(0)
+    bad_ptr = C.byref(bad) if check_finite else None
     with torch.cuda.device(s3.device):
-        rc = lib().cf_wmc_filter_u8_f32(
-            s3.data_ptr(), W, H * W, out.data_ptr(), W, H, W, P, H * W, int(cfg.iters),
-            float(cfg.dt), workspace.data_ptr() if workspace is not None else None,
-            nbytes if workspace is not None else 0, C.byref(bad) if check_finite else None,
-            _stream_ptr(torch, s3.device))
+        strm = _stream_ptr(torch, s3.device)
+        if out_dtype == "u8":
+            rc = lib().cf_wmc_filter_u8_u8(s3.data_ptr(), W, H * W, out.data_ptr(), W, H * W, W, H,
+                                           P, int(cfg.iters), float(cfg.dt), ptr(workspace),
+                                           nbytes, bad_ptr, strm)
+        else:
+            rc = lib().cf_wmc_filter_u8_f32(s3.data_ptr(), W, H * W, out.data_ptr(), W, H, W, P,
+                                            H * W, int(cfg.iters), float(cfg.dt), ptr(workspace),
+                                            nbytes if workspace is not None else 0, bad_ptr, strm)
     if rc == CF_ENONFINITE:
         raise FlowError(bad.value)
     check(rc, "mc_flow_u8")
