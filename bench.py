@@ -367,6 +367,36 @@ def bench_b200(args, cfg):
                      "bitwise_equal": same}
         assert same, "self-check failed: the timed output differs from an alternative schedule"
         del cur, nxt
+    elif world > 1 and cfg.sharding == "rows" and cfg.iters > 0:
+        # N > 1: gather the bands to rank 0 and compare with one GPU's filter
+        # of the same input (whatever the halo transport, NCCL or IPC)
+        if args.halo == "ipc":
+            step()
+            band = torch.empty((lay.r1 - lay.r0, cfg.w), dtype=torch.float32, device=dev)
+            src_ptr = flow._row_ptr(flow.bufs[ipc_result[0]], lay.buf_row0, lay.r0)
+            assert L.cf_copy(band.data_ptr(), src_ptr, band.numel() * 4, sp) == 0
+        else:
+            band = step()[lay.band_slice()].clone()
+        torch.cuda.synchronize(dev)
+        maxr = max(r1 - r0 for r0, r1 in sharded.band_bounds(cfg.h, world))
+        pad = torch.zeros((maxr, cfg.w), dtype=torch.float32, device=dev)
+        pad[:band.shape[0]] = band
+        on = dev if backend == "nccl" else "cpu"
+        parts = [torch.empty((maxr, cfg.w), dtype=torch.float32, device=on)
+                 for _ in range(world)]
+        dist.all_gather(parts, pad.to(on))
+        if rank == 0:
+            full_in = torch.from_numpy(make_input(cfg)).to(dev)
+            ref_out = cf.mc_flow(full_in, cf.FlowConfig(dt=cfg.dt, iters=cfg.iters),
+                                 inplace=True, check_finite=False)
+            got = torch.cat([parts[q][:r1 - r0].to(dev) for q, (r0, r1)
+                             in enumerate(sharded.band_bounds(cfg.h, world))])
+            same = bool(torch.equal(got.view(torch.int32), ref_out.view(torch.int32)))
+            selfcheck = {"reference": "single-GPU filter of the same input on rank 0 "
+                                      "(no oracle)", "bitwise_equal": same}
+            assert same, "self-check failed: sharded result differs from the single-GPU filter"
+            del full_in, ref_out, got
+        del parts, pad, band
     updates_job = cfg.updates  # whole job over all ranks (strong scaling for rows)
     if world > 1 and cfg.sharding == "images":
         updates_job = updates_local * world  # per-rank fixed share (weak scaling)
