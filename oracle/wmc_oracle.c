@@ -33,6 +33,22 @@
  * blocks, one per worker, caller runs block 0, serial if height < 16 or one
  * worker.  Output is bit-identical for any thread count (parallel.hpp:23-25).
  *
+ * Also restated: solve_l2_area / solve_l1_area (the fp32
+ * sequences of DESIGN.md §3.5), the WMC energy, fidelity sums and histogram
+ * in the fixed reduction order of csrc/wmc_reduce.cu, 8-bit widening and
+ * save-time quantisation.
+ *
+ * Pinning (the reference has no tests, fixtures or golden files for this
+ * path -- only its spec and proj/include/curveflow/parallel.hpp): the oracle
+ * is pinned by the spec's own examples and acceptance criteria
+ * (tests/test_oracle.py: kernel exactness, 1000 random 8x8 vs a naive double
+ * loop, constant / impulse / ramp / affine known answers, homogeneity and
+ * shift, flow identity / max principle / non-finite naming, the l1 algebra
+ * KATs and identity, lambda-sweep SSIM ordering), by golden vectors from
+ * independent pure-Python / numpy transcriptions (tests/golden/), and by the
+ * fp64 restatement run on the reference's own executor (oracle/_ref/,
+ * bit-identical).
+ *
  * Build: oracle/Makefile, gcc -O2 -ffp-contract=off (no -ffast-math), SSE
  * arithmetic (x86-64 default), so every + and * rounds once to the declared
  * type and fmaf()/fma() are the only fused operations.
