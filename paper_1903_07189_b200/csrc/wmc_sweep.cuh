@@ -226,6 +226,12 @@ __device__ __forceinline__ void cp_async_wait_rd() {
 // The C+2 pairs (columns C*i-1 .. C*i+C) a lane needs from one row, read
 // with 16-byte LDS from byte a = row + 8*C*i (16-aligned).
 __device__ __forceinline__ void lds_nb(uint32_t a, f2 (&q)[C + 2]) {
+#ifdef CF_EXP_NO_LDS  // diagnostic only (wrong results): cost of the ring loads
+#pragma unroll
+    for (int k = 0; k < C + 2; ++k)
+        asm volatile("mov.b64 %0, {%1, %2};" : "=l"(q[k]) : "r"(a + k), "r"(a ^ k));
+    return;
+#endif
 #pragma unroll
     for (int k = 0; k < (C + 2) / 2; ++k) {
 #ifndef CF_SCALAR
