@@ -78,9 +78,9 @@ int device_info(DevInfo* out) {
     return CF_OK;
 }
 
-template <int K>
+template <int K, int MODE>
 constexpr size_t smem_bytes() {
-    return (size_t)cfk::kWarpsPerBlock * cfk::smem_bytes_per_warp<K>();
+    return (size_t)cfk::kWarpsPerBlock * cfk::smem_bytes_per_warp<K, MODE>();
 }
 
 template <int K, int MODE>
@@ -91,12 +91,12 @@ int kernel_occupancy_warps() {
     static std::atomic<int> cached{-1};
     int v = cached.load(std::memory_order_acquire);
     if (v < 0) {
-        if (smem_bytes<K>() > 48 * 1024)
+        if (smem_bytes<K, MODE>() > 48 * 1024)
             cudaFuncSetAttribute(cfk::wmc_sweeps_kernel<K, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<K>());
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<K, MODE>());
         int blocks = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &blocks, cfk::wmc_sweeps_kernel<K, MODE>, cfk::kThreads, smem_bytes<K>()) !=
+                &blocks, cfk::wmc_sweeps_kernel<K, MODE>, cfk::kThreads, smem_bytes<K, MODE>()) !=
                 cudaSuccess ||
             blocks <= 0)
             blocks = 2;
@@ -168,7 +168,7 @@ int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
     const int64_t tasks = (nb * p.n_strips_b + (n_pairs - nb) * p.n_strips) * p.planes;
     const int64_t blocks = (tasks + cfk::kWarpsPerBlock - 1) / cfk::kWarpsPerBlock;
     if (blocks > INT_MAX) return CF_EINVAL;
-    cfk::wmc_sweeps_kernel<K, MODE><<<(unsigned)blocks, cfk::kThreads, smem_bytes<K>(), s>>>(p);
+    cfk::wmc_sweeps_kernel<K, MODE><<<(unsigned)blocks, cfk::kThreads, smem_bytes<K, MODE>(), s>>>(p);
     CF_CUDA(cudaGetLastError());
     return CF_OK;
 }

@@ -141,9 +141,22 @@ struct Geo {
 // Rings: level 0 has kRS slots (rows t-2 .. t+RD); levels 1..K-1 have 4
 // slots each (skewed pipeline).
 constexpr int kLvlSlots = 4;
+// Solver modes stage the data term f in a third ring (kFSlots rows, each lane's
+// own C column pairs only, 16-byte aligned): rows t-(2K-1) .. t+RD are live.
+constexpr int kFSlots = 16;
+constexpr int kFRowBytes = 8 * 32 * CF_COLS;
+// kModeL1 also stages the incoming dual d (read by level 1 only: rows
+// t-1 .. t+RD live).
+constexpr int kDSlots = 8;
 template <int K>
-__host__ __device__ constexpr int smem_bytes_per_warp() {
+__host__ __device__ constexpr int ring_bytes_per_warp() {
     return (kRS + kLvlSlots * (K - 1)) * kRowBytes;
+}
+template <int K, int MODE>
+__host__ __device__ constexpr int smem_bytes_per_warp() {
+    static_assert(2 * K + CF_RD <= kFSlots && CF_RD + 2 <= kDSlots, "data-term rings too small");
+    return ring_bytes_per_warp<K>() + (MODE >= 2 ? kFSlots * kFRowBytes : 0) +  // kModeL2/L1
+           (MODE == 3 ? kDSlots * kFRowBytes : 0);                               // kModeL1
 }
 
 // ---------------------------------------------------------------------------
@@ -371,6 +384,7 @@ struct SweepWarp {
     float* ddp;                   // plane base of d^{t+K} (kModeL1)
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
+    uint32_t fbase;               // this lane's slice of the data-term ring (solver modes)
     f2 acc[K + 1][C];             // non-finite accumulators per level and column
     // Row sums l+r and (a+c)+(l+r) carried down a level from the row above
     // (K <= 2), or recomputed (K >= 3: the 16 registers buy occupancy there;
@@ -412,6 +426,8 @@ struct SweepWarp {
     __device__ __forceinline__ void prefetch(int y) const {
         const float* row = srcp + (int64_t)(y - P.src_row0) * P.src_pitch;
         const uint32_t s = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
+        const float* frow = nullptr;
+        if constexpr (kFRing) frow = fp + (int64_t)y * P.f_pitch;
 #pragma unroll
         for (int j = 0; j < C; ++j) {
             int x0 = xf[0] + j, x1 = xf[1] + j;
@@ -421,8 +437,40 @@ struct SweepWarp {
             }
             cp_async4(s + 8 * j, row + x0);
             cp_async4(s + 8 * j + 4, row + x1);
+            if constexpr (kFRing) {
+                const uint32_t fs = fslot(y) + 8 * j;
+                cp_async4(fs, frow + x0);
+                cp_async4(fs + 4, frow + x1);
+            }
+            if constexpr (MODE == kModeL1) {
+                const float* drow = dsp + (int64_t)y * P.f_pitch;
+                const uint32_t ds = dslot(y) + 8 * j;
+                cp_async4(ds, drow + x0);
+                cp_async4(ds + 4, drow + x1);
+            }
         }
     }
+
+    // Data-term ring (solver modes): this lane's slot of row y, and the pair
+    // {f[y][xf[0]+jj], f[y][xf[1]+jj]} from it.
+    static constexpr bool kFRing = MODE == kModeL2 || MODE == kModeL1;
+    __device__ __forceinline__ uint32_t fslot(int y) const {
+        return fbase + (uint32_t)(y & (kFSlots - 1)) * kFRowBytes;
+    }
+    __device__ __forceinline__ uint32_t dslot(int y) const {
+        return fbase + (uint32_t)(kFSlots + (y & (kDSlots - 1))) * kFRowBytes;
+    }
+    static __device__ __forceinline__ f2 lds_pair(uint32_t a) {
+        f2 v;
+#ifndef CF_SCALAR
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+#else
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+#endif
+        return v;
+    }
+    __device__ __forceinline__ f2 ld_f(int y, int jj) const { return lds_pair(fslot(y) + 8 * jj); }
+    __device__ __forceinline__ f2 ld_d(int y, int jj) const { return lds_pair(dslot(y) + 8 * jj); }
 
     // Clamp-to-edge at the image's left / right column (border warps): the
     // pixel at x = 0 takes its own column as its x-1 neighbours (a <- b,
@@ -445,19 +493,6 @@ struct SweepWarp {
         }
     }
 
-    // Pointwise pair {plane[y][xf[0]+jj], plane[y][xf[1]+jj]} of an f-geometry
-    // plane (data term / dual); CHECKED clamps the columns (checked steps and
-    // the border warps' edge steps).
-    template <bool CHECKED>
-    __device__ __forceinline__ f2 ld_pt(const float* plane, int y, int jj) const {
-        const float* row = plane + (int64_t)y * P.f_pitch;
-        int x0 = xf[0] + jj, x1 = xf[1] + jj;
-        if (CHECKED) {
-            x0 = min(max(x0, 0), P.w - 1);
-            x1 = min(max(x1, 0), P.w - 1);
-        }
-        return pk(__ldg(row + x0), __ldg(row + x1));
-    }
 
     // Compute level L's row for step t.  CHECKED: range check, clamped row
     // indices, predicated stores.  Fast: steady state, rows via R4[] (slot
@@ -538,7 +573,7 @@ struct SweepWarp {
                 nv[j - 1] = hw;
             } else if constexpr (MODE == kModeL2) {
                 // SPEC.md:298 with A = I: U' = U + dt*((f - U) + lambda*H^w(U))
-                const f2 fv = ld_pt<CHECKED || EDGE>(fp, y, j - 1);
+                const f2 fv = ld_f(y, j - 1);
                 const f2 r = fma2(o[j], splat(-1.0f), fv);         // f - u
                 const f2 sdir = fma2(splat(P.lambda), hw, r);      // (f-u) + lambda*H
                 nv[j - 1] = fma2(splat(P.dt), sdir, o[j]);
@@ -547,9 +582,9 @@ struct SweepWarp {
                 // SPEC.md:306 with A = I:
                 //   r = (u - f) + d;  d' = clamp(r, -alpha, alpha)
                 //   U' = u + dt*(lambda*H^w - (2d' - d)/alpha)
-                const f2 fv = ld_pt<CHECKED || EDGE>(fp, y, j - 1);
+                const f2 fv = ld_f(y, j - 1);
                 f2 dv;
-                if constexpr (L == 1) dv = ld_pt<CHECKED || EDGE>(dsp, y, j - 1);
+                if constexpr (L == 1) dv = ld_d(y, j - 1);
                 else dv = dold[L - 1][j - 1];
                 const f2 r = add2(fma2(fv, splat(-1.0f), o[j]), dv);
                 const f2 dn = pk(fminf(fmaxf(lo(r), -P.alpha), P.alpha),
@@ -740,6 +775,24 @@ struct SweepWarp {
                     cp_async4(sa + 8 * j, lptr + j);
                     cp_async4(sa + 8 * j + 4, lptr + G::S + j);
                 }
+                if constexpr (kFRing) {  // interior warp: both chunks present
+                    const float* frow = fp + (int64_t)(t + kRD) * P.f_pitch + xf[0];
+                    const uint32_t fs = fslot(t + kRD);
+#pragma unroll
+                    for (int j = 0; j < C; ++j) {
+                        cp_async4(fs + 8 * j, frow + j);
+                        cp_async4(fs + 8 * j + 4, frow + G::S + j);
+                    }
+                }
+                if constexpr (MODE == kModeL1) {
+                    const float* drow = dsp + (int64_t)(t + kRD) * P.f_pitch + xf[0];
+                    const uint32_t ds = dslot(t + kRD);
+#pragma unroll
+                    for (int j = 0; j < C; ++j) {
+                        cp_async4(ds + 8 * j, drow + j);
+                        cp_async4(ds + 8 * j + 4, drow + G::S + j);
+                    }
+                }
             } else {
                 prefetch(t + kRD);
             }
@@ -851,8 +904,9 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
     sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
     sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
-               (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K>();
+               (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K, MODE>();
     sw.lbase = sw.sbase + 8 * C * sw.lane;
+    sw.fbase = sw.sbase + ring_bytes_per_warp<K>() + 8 * C * sw.lane;
 
     sw.run();
 
