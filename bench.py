@@ -294,7 +294,8 @@ def bench_b200(args, cfg):
                 rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, cfg.iters, cfg.dt,
                                          ws.data_ptr(), nbytes, None, cur_sp())
                 assert rc == 0, rc
-        launches_per_step = int(L.cf_wmc_filter_launches(W, H, P, cfg.iters)) + (2 if cfg.u8
+        # u8: + the widening kernel (the re-quantisation is fused into the last sweep)
+        launches_per_step = int(L.cf_wmc_filter_launches(W, H, P, cfg.iters)) + (1 if cfg.u8
                                                                                  else 0)
 
     def barrier():

@@ -322,10 +322,16 @@ struct DataTerm {            // solve_l2_area / solve_l1_area (f != nullptr)
     float alpha = 1.0f;
 };
 
+struct Out8 {               // fused save-time quantisation of the last launch
+    uint8_t* p = nullptr;
+    int64_t pitch = 0, plane = 0;
+};
+
 static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t src_plane,
                     float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
                     int64_t plane_stride, int32_t iters, float dt, void* workspace,
-                    int32_t* first_bad_iter, cudaStream_t s, DataTerm dterm = {}) {
+                    int32_t* first_bad_iter, cudaStream_t s, DataTerm dterm = {},
+                    Out8 out8 = {}) {
     DevInfo d;
     if (int rc = device_info(&d)) return rc;
     int32_t* flag = reinterpret_cast<int32_t*>(workspace);
@@ -359,6 +365,9 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
         p.fdata = dterm.f; p.f_pitch = pitch; p.f_plane = plane_stride; p.lambda = dterm.lambda;
         p.dsrc = dcur; p.ddst = dnxt;
         p.alpha = dterm.alpha; p.neg_inv_alpha = -(1.0f / dterm.alpha);
+        if (out8.p && i + 1 == ks.size()) {  // last launch: u8 bytes instead of fp32
+            p.dst8 = out8.p; p.dst8_pitch = out8.pitch; p.dst8_plane = out8.plane;
+        }
         const int rc = dterm.d   ? launch<cfk::kModeL1>(p, ks[i], d, s)
                        : dterm.f ? launch<cfk::kModeL2>(p, ks[i], d, s)
                                  : launch<cfk::kModeFlow>(p, ks[i], d, s);
@@ -367,7 +376,7 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
         std::swap(cur, nxt);
         std::swap(dcur, dnxt);
     }
-    if (cur != out) {
+    if (cur != out && !out8.p) {
         // iters == 1 on an in-place f32 image: the single launch wrote ws
         for (int pl = 0; pl < planes; ++pl)
             CF_CUDA(cudaMemcpy2DAsync(out + pl * plane_stride, pitch * 4, cur + pl * plane_stride,
@@ -380,6 +389,20 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
     }
     if (first_bad_iter) return cf_wmc_filter_query_nonfinite(workspace, first_bad_iter, s);
     return CF_OK;
+}
+
+// u8 frames in, u8 frames out with the quantisation fused into the last
+// launch (wmc_io.cu's cf_wmc_filter_u8_u8; arguments validated there).
+// fbuf: dense fp32 planes (pitch w), fws: the filter workspace.
+extern "C" int cf_internal_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_plane,
+                                        float* fbuf, int32_t w, int32_t h, int32_t planes,
+                                        int32_t iters, float dt, void* fws, uint8_t* out,
+                                        int64_t out_pitch, int64_t out_plane,
+                                        int32_t* first_bad_iter, void* stream) {
+    Out8 o8;
+    o8.p = out; o8.pitch = out_pitch; o8.plane = out_plane;
+    return run_flow(in, true, in_pitch, in_plane, fbuf, w, h, w, planes, (int64_t)w * h, iters,
+                    dt, fws, first_bad_iter, (cudaStream_t)stream, DataTerm{}, o8);
 }
 
 CF_API int cf_wmc_filter_f32(float* img, int32_t w, int32_t h, int64_t pitch, int32_t planes,

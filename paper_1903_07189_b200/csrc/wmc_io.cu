@@ -16,6 +16,11 @@
 #include "../../include/curveflow/capi.h"
 
 extern "C" void cf_internal_set_cuda_error(int e);  // wmc_capi.cu (not exported)
+extern "C" int cf_internal_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_plane,
+                                        float* fbuf, int32_t w, int32_t h, int32_t planes,
+                                        int32_t iters, float dt, void* fws, uint8_t* out,
+                                        int64_t out_pitch, int64_t out_plane,
+                                        int32_t* first_bad_iter, void* stream);
 
 namespace {
 
@@ -155,9 +160,14 @@ CF_API int cf_wmc_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_p
     const int64_t plane = (int64_t)w * h;
     float* f = reinterpret_cast<float*>(workspace);
     const size_t off = align256((size_t)(planes * plane) * sizeof(float));
-    int rc = cf_wmc_filter_u8_f32(in, in_pitch, in_plane_stride, f, w, h, w, planes, plane, iters,
-                                  dt, reinterpret_cast<char*>(workspace) + off,
-                                  workspace_bytes - off, first_bad_iter, stream);
+    if (!(dt > 0.0f) || dt > 1.0f) return CF_EINVAL;
+    if (iters > 0)  // the last sweep launch stores quantised bytes (no fp32 round trip)
+        return cf_internal_filter_u8_u8(in, in_pitch, in_plane_stride, f, w, h, planes, iters, dt,
+                                        reinterpret_cast<char*>(workspace) + off, out, out_pitch,
+                                        out_plane_stride, first_bad_iter, stream);
+    int rc = cf_wmc_filter_u8_f32(in, in_pitch, in_plane_stride, f, w, h, w, planes, plane, 0, dt,
+                                  reinterpret_cast<char*>(workspace) + off, workspace_bytes - off,
+                                  first_bad_iter, stream);
     if (rc) return rc;
     quantize_planes_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(
         f, w, plane, w, h, planes, out, out_pitch, out_plane_stride);

@@ -112,6 +112,11 @@ struct SweepParams {
     float* peer_up;
     float* peer_dn;
     int32_t peer_up_row0, peer_up_end, peer_dn_row0, peer_dn_begin;
+    // Fused save-time quantisation (kModeFlow, the u8 -> u8 path's last
+    // launch): level-K rows go to dst8 as rint(clamp(v,0,1)*255) bytes
+    // instead of fp32 to dst.  Null: fp32 output.
+    uint8_t* dst8;
+    int64_t dst8_pitch, dst8_plane;
     // MODE == kModeL2 (solve_l2_area): data term f and lambda
     const float* fdata;       // global row 0 of plane 0 (same column geometry as src)
     int64_t f_pitch, f_plane; // elements
@@ -124,6 +129,12 @@ struct SweepParams {
 };
 
 // Per-pixel update a launch applies at every level.
+// Save-time quantisation, shared with csrc/wmc_io.cu.
+__device__ __forceinline__ uint8_t quantize_u8(float v) {
+    const float c = fminf(fmaxf(v, 0.0f), 1.0f);  // NaN -> 0 (fmaxf returns the number)
+    return (uint8_t)__float2int_rn(__fmul_rn(c, 255.0f));
+}
+
 constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_flow)
 constexpr int kModeMap = 1;   // out = H^w(U), one level, fp64 near-tie rule (wmc_half_laplace)
 constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)
@@ -382,6 +393,7 @@ struct SweepWarp {
     const float* fp;              // plane base of f (kModeL2, kModeL1)
     const float* dsp;             // plane base of d^t (kModeL1)
     float* ddp;                   // plane base of d^{t+K} (kModeL1)
+    uint8_t* d8p;                 // plane base of the u8 output (fused quantisation)
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
     uint32_t fbase;               // this lane's slice of the data-term ring (solver modes)
@@ -612,6 +624,16 @@ struct SweepWarp {
         if constexpr (L < K) store<L + 1, CHECKED, EDGE>(t, R4, sptr);
     }
 
+    // This lane's output columns of a level-K row as quantised bytes.
+    __device__ __forceinline__ void store_row8(uint8_t* row, const f2 (&nv)[C]) const {
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            if (!outc[j]) continue;
+            if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = quantize_u8(lo(nv[j]));
+            if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = quantize_u8(hi(nv[j]));
+        }
+    }
+
     // This lane's output columns of a level-K row (bounds-checked).
     __device__ __forceinline__ void store_row(float* row, const f2 (&nv)[C]) const {
 #pragma unroll
@@ -636,6 +658,12 @@ struct SweepWarp {
                     drow[xf[0] + j] = lo(odv[K][j]);
                 if (out_h[1] && (!(CHECKED || EDGE) || xf[1] + j < P.w))
                     drow[xf[1] + j] = hi(odv[K][j]);
+            }
+        }
+        if constexpr (L == K && MODE == kModeFlow) {
+            if (d8p) {  // u8 output (warp-uniform): quantise in the store
+                store_row8(d8p + (int64_t)(y - P.dst_row0) * P.dst8_pitch, nv);
+                return;
             }
         }
         if constexpr (L == K) {
@@ -903,6 +931,7 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
     sw.fp = (MODE == kModeL2 || MODE == kModeL1) ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
     sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
     sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
+    sw.d8p = (MODE == kModeFlow && p.dst8) ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K, MODE>();
     sw.lbase = sw.sbase + 8 * C * sw.lane;
