@@ -370,6 +370,7 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
         }
         const int rc = dterm.d   ? launch<cfk::kModeL1>(p, ks[i], d, s)
                        : dterm.f ? launch<cfk::kModeL2>(p, ks[i], d, s)
+                       : p.dst8  ? launch<cfk::kModeFlowU8>(p, ks[i], d, s)
                                  : launch<cfk::kModeFlow>(p, ks[i], d, s);
         if (rc) return rc;
         iter += ks[i];

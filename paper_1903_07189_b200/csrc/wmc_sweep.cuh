@@ -112,9 +112,9 @@ struct SweepParams {
     float* peer_up;
     float* peer_dn;
     int32_t peer_up_row0, peer_up_end, peer_dn_row0, peer_dn_begin;
-    // Fused save-time quantisation (kModeFlow, the u8 -> u8 path's last
+    // Fused save-time quantisation (kModeFlowU8, the u8 -> u8 path's last
     // launch): level-K rows go to dst8 as rint(clamp(v,0,1)*255) bytes
-    // instead of fp32 to dst.  Null: fp32 output.
+    // instead of fp32 to dst.
     uint8_t* dst8;
     int64_t dst8_pitch, dst8_plane;
     // MODE == kModeL2 (solve_l2_area): data term f and lambda
@@ -139,6 +139,7 @@ constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_f
 constexpr int kModeMap = 1;   // out = H^w(U), one level, fp64 near-tie rule (wmc_half_laplace)
 constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)
 constexpr int kModeL1 = 3;    // primal-dual step of solve_l1_area
+constexpr int kModeFlowU8 = 4;  // kModeFlow whose level-K rows are stored as u8 bytes
 
 // Column geometry for K levels: each chunk window overlaps its neighbours by
 // A = K columns per side (the trapezoid shrinks one column per level).
@@ -166,8 +167,8 @@ __host__ __device__ constexpr int ring_bytes_per_warp() {
 template <int K, int MODE>
 __host__ __device__ constexpr int smem_bytes_per_warp() {
     static_assert(2 * K + CF_RD <= kFSlots && CF_RD + 2 <= kDSlots, "data-term rings too small");
-    return ring_bytes_per_warp<K>() + (MODE >= 2 ? kFSlots * kFRowBytes : 0) +  // kModeL2/L1
-           (MODE == 3 ? kDSlots * kFRowBytes : 0);                               // kModeL1
+    return ring_bytes_per_warp<K>() + ((MODE == 2 || MODE == 3) ? kFSlots * kFRowBytes : 0) +
+           (MODE == 3 ? kDSlots * kFRowBytes : 0);  // f ring: kModeL2/L1; d ring: kModeL1
 }
 
 // ---------------------------------------------------------------------------
@@ -660,11 +661,9 @@ struct SweepWarp {
                     drow[xf[1] + j] = hi(odv[K][j]);
             }
         }
-        if constexpr (L == K && MODE == kModeFlow) {
-            if (d8p) {  // u8 output (warp-uniform): quantise in the store
-                store_row8(d8p + (int64_t)(y - P.dst_row0) * P.dst8_pitch, nv);
-                return;
-            }
+        if constexpr (L == K && MODE == kModeFlowU8) {  // quantise in the store
+            store_row8(d8p + (int64_t)(y - P.dst_row0) * P.dst8_pitch, nv);
+            return;
         }
         if constexpr (L == K) {
             if (CHECKED || EDGE) {
@@ -859,9 +858,10 @@ struct SweepWarp {
 template <int K, int MODE>
 // The solver modes carry f (and the dual FIFO): 3 blocks/SM = 168 registers,
 // no spills at the filter's K = 2.
-__global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
-                                           : (MODE == kModeFlow && K == 2)     ? CF_MINB_EVEN
-                                                                               : CF_MINB)
+__global__ void __launch_bounds__(kThreads,
+                                  (MODE == kModeL2 || MODE == kModeL1)                    ? 3
+                                  : ((MODE == kModeFlow || MODE == kModeFlowU8) && K == 2) ? CF_MINB_EVEN
+                                                                                           : CF_MINB)
     wmc_sweeps_kernel(const SweepParams p) {
     constexpr bool MAP = MODE == kModeMap;
     using G = Geo<K>;
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, MODE >= kModeL2                  ? 3
     sw.fp = (MODE == kModeL2 || MODE == kModeL1) ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
     sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
     sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
-    sw.d8p = (MODE == kModeFlow && p.dst8) ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
+    sw.d8p = MODE == kModeFlowU8 ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K, MODE>();
     sw.lbase = sw.sbase + 8 * C * sw.lane;
