@@ -672,3 +672,35 @@ def test_fuzz_large_geometries():
         ref, bad = oracle.flow_f32(src, iters, dt)
         assert bad == 0
         assert_bitexact(out, ref, f"large fuzz {P}x{h}x{w} it {iters} dt {dt}")
+
+
+@pytest.mark.parametrize("dt", [1e-7, 1e-3, 0.999, 1.0])
+def test_flow_extreme_dt(dt):
+    img = cf.synth_image(150, 333, seed=8, n_rects=10, n_discs=10, sigma=0.1)
+    got = cf.mc_flow(torch.from_numpy(img).cuda(), cf.FlowConfig(dt=dt, iters=9)).cpu().numpy()
+    ref, bad = oracle.flow_f32(img, 9, dt)
+    assert bad == 0
+    assert_bitexact(got, ref, f"dt={dt}")
+
+
+@pytest.mark.parametrize("model,lam,alpha,dt", [("l2_area", 1e4, 1.0, 1e-5),
+                                                ("l1_area", 5.0, 1e-20, 0.15),
+                                                ("l1_area", 1e-6, 1e6, 0.9)])
+def test_solver_extreme_parameters(model, lam, alpha, dt):
+    """Huge lambda with a tiny step, alpha small enough that 1/alpha
+    overflows the dual step (divergence must be named at the oracle's
+    iteration), and a huge alpha: GPU == oracle bit for bit."""
+    f = cf.synth_image(90, 260, seed=12, n_rects=6, n_discs=6, sigma=0.1)
+    iters = 7
+    if model == "l1_area":
+        ref, ref_d, bad = oracle.solve_l1_area_f32(f, iters, dt, lam, alpha)
+    else:
+        ref, bad = oracle.solve_l2_area_f32(f, iters, dt, lam)
+    cfg = cf.SolverConfig(model=model, lam=lam, alpha=alpha, dt=dt, iters=iters)
+    if bad:
+        with pytest.raises(cf.FlowError) as e:
+            cf.solve(torch.from_numpy(f).cuda(), cfg)
+        assert e.value.iteration == bad
+        return
+    rep = cf.solve(torch.from_numpy(f).cuda(), cfg)
+    assert_bitexact(rep.image.cpu().numpy(), ref, f"{model} lam={lam} alpha={alpha}")
