@@ -460,29 +460,32 @@ def bench_b200(args, cfg):
 
     # ---------------- end-to-end through the public API, host buffers ----------
     # Every step copies its input from pinned host memory and reads its result
-    # back.  Copies run on two copy streams, double-buffered, so step i's D2H
+    # back.  Copies run on two copy streams, triple-buffered, so step i's D2H
     # and step i+1's H2D overlap step i+1's / i's compute (a streaming user's
     # pipeline); the filter itself is the public mc_flow / mc_flow_u8 /
     # wmc_half_laplace call on the compute stream.
     pipelined = not (world > 1 and cfg.sharding == "rows")
     if pipelined:
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        dbufs = [torch.empty(host_t.shape, dtype=host_t.dtype, device=dev) for _ in range(2)]
-        obufs = [torch.empty(out_host.shape, dtype=out_dtype, device=dev) for _ in range(2)]
+        # triple-buffered: step i+1's H2D goes to a buffer whose D2H (step
+        # i-2) finished long ago, so it overlaps step i's compute entirely
+        NB = 3
+        dbufs = [torch.empty(host_t.shape, dtype=host_t.dtype, device=dev) for _ in range(NB)]
+        obufs = [torch.empty(out_host.shape, dtype=out_dtype, device=dev) for _ in range(NB)]
         ws_e2e = int(L.cf_wmc_filter_u8_u8_workspace_bytes(W, H, P) if cfg.u8 else
                      L.cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
         flag_off = (P * H * W * 4 + 255) // 256 * 256 if cfg.u8 else 0
-        wss = [torch.empty(ws_e2e, dtype=torch.uint8, device=dev) for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+        wss = [torch.empty(ws_e2e, dtype=torch.uint8, device=dev) for _ in range(NB)]
+        ev_out = [torch.cuda.Event() for _ in range(NB)]
         for e in ev_out:
             e.record(s_out)
-        flag_host = torch.zeros(2, dtype=torch.int32).pin_memory()
+        flag_host = torch.zeros(NB, dtype=torch.int32).pin_memory()
         e2e_i = [0]
 
         def e2e_step():
             i = e2e_i[0]
             e2e_i[0] += 1
-            b = i % 2
+            b = i % NB
             with torch.cuda.stream(s_in):
                 s_in.wait_event(ev_out[b])           # buffer b's previous D2H done
                 dbufs[b].copy_(host_t, non_blocking=True)
@@ -582,7 +585,7 @@ def bench_b200(args, cfg):
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4), "steps": e2e_steps,
                 "pipeline": ("H2D/D2H from pinned host memory every step on two copy streams, "
-                             "double-buffered against the compute stream" if pipelined else
+                             "triple-buffered against the compute stream" if pipelined else
                              "sequential H2D, filter, D2H")},
         "gpu_launches": launches_per_step * args.steps,
         "selfcheck": selfcheck,
