@@ -611,7 +611,7 @@ def bench_b200(args, cfg):
             "l2": ("inputs larger than L2 (126 MB)" if not l2_resident else
                    "working set fits in L2: 256 MiB flush between timed steps"),
             "timing": ("one CUDA graph per step, CUDA events per step" if graph else
-                       "CUDA events around the step loop, max over ranks"),
+                       "CUDA events per step (summed), max over ranks"),
         },
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4), "steps": e2e_steps,
