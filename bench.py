@@ -342,6 +342,8 @@ def bench_b200(args, cfg):
         run_step = g.replay
     with ClockSampler(local) as clk:
         ms_step = timed(run_step, args.steps)
+    if world > 1 and cfg.sharding == "rows" and args.halo != "ipc":
+        assert int(flag.item()) == 0x7F7F7F7F, f"non-finite value in band launch {flag.item()}"
     if ws is not None:  # device non-finite flag of the last timed step
         import ctypes
         bad = ctypes.c_int32(0)
