@@ -1,11 +1,14 @@
 """GPU parity: the sm_100a kernels through the C-ABI vs the fp32 canonical
 oracle (bit-exact) and the fp64 SPEC-faithful oracle (<= 1e-5)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import paper_1903_07189_b200 as cf
+from paper_1903_07189_b200._lib import CF_ENONFINITE
 
 pytestmark = pytest.mark.gpu
 
@@ -704,3 +707,140 @@ def test_solver_extreme_parameters(model, lam, alpha, dt):
         return
     rep = cf.solve(torch.from_numpy(f).cuda(), cfg)
     assert_bitexact(rep.image.cpu().numpy(), ref, f"{model} lam={lam} alpha={alpha}")
+
+
+def _graph_cache_rounds(run, make_input, ref, rounds=4):
+    """Same buffers, new contents each call: call 1 launches directly, call 2
+    captures the launch graph, calls 3+ replay it (wmc_capi.cu run_cached)."""
+    for r in range(rounds):
+        inp = make_input(r)
+        got = run(inp)
+        torch.cuda.synchronize()
+        for g, e, what in zip(got, ref(inp), ("U", "d")):
+            if g.dtype == np.uint8:
+                assert np.array_equal(g, e), f"graph-cache round {r} {what}"
+            else:
+                assert_bitexact(g, e, f"graph-cache round {r} {what}")
+
+
+@pytest.mark.parametrize("side_stream", [False, True])
+@pytest.mark.parametrize("iters", [1, 7, 20])
+def test_graph_cache_filter_f32(side_stream, iters):
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    P, h, w = 2, 70, 333
+    x = torch.empty((P, h, w), device="cuda")
+    nb = int(L.cf_wmc_filter_workspace_bytes(w, h, w, P, h * w))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream() if side_stream else torch.cuda.default_stream()
+    bad = C.c_int32(-1)
+
+    def make(r):
+        return np.stack([cf.synth_image(h, w, seed=900 + 10 * r + p, n_rects=5, n_discs=5,
+                                        sigma=0.1) for p in range(P)])
+
+    def run(a):
+        with torch.cuda.stream(stream):
+            x.copy_(torch.from_numpy(a))
+            rc = L.cf_wmc_filter_f32(x.data_ptr(), w, h, w, P, h * w, iters, 0.7, ws.data_ptr(),
+                                     nb, C.byref(bad), stream.cuda_stream)
+        assert rc == 0 and bad.value == 0
+        return (x.cpu().numpy(),)
+
+    _graph_cache_rounds(run, make, lambda a: (oracle.flow_f32(a, iters, 0.7)[0],))
+
+
+def test_graph_cache_nonfinite_flag_resets():
+    """The flag reset (memset) is inside the captured graph: a replay after a
+    non-finite run reports clean again, and a non-finite replay is caught."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    h, w, iters = 40, 90, 6
+    x = torch.empty((h, w), device="cuda")
+    nb = int(L.cf_wmc_filter_workspace_bytes(w, h, w, 1, h * w))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bad = C.c_int32(-1)
+    clean = cf.synth_image(h, w, seed=5, n_rects=3, n_discs=3, sigma=0.1)
+    dirty = clean.copy()
+    dirty[20, 45] = np.inf
+    for r, a in enumerate([clean, clean, dirty, clean, dirty, clean]):
+        x.copy_(torch.from_numpy(a))
+        rc = L.cf_wmc_filter_f32(x.data_ptr(), w, h, w, 1, h * w, iters, 1.0, ws.data_ptr(), nb,
+                                 C.byref(bad), torch.cuda.current_stream().cuda_stream)
+        ref, ref_bad = oracle.flow_f32(a, iters, 1.0)
+        if ref_bad:
+            assert rc == CF_ENONFINITE and bad.value == ref_bad, f"round {r}"
+        else:
+            assert rc == 0 and bad.value == 0, f"round {r}"
+            assert_bitexact(x.cpu().numpy(), ref, f"flag round {r}")
+
+
+def test_graph_cache_u8_and_l1():
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    P, h, w, iters = 3, 50, 201, 9
+    q_d = torch.empty((P, h, w), dtype=torch.uint8, device="cuda")
+    o_d = torch.empty_like(q_d)
+    nb8 = int(L.cf_wmc_filter_u8_u8_workspace_bytes(w, h, P))
+    ws8 = torch.empty(nb8, dtype=torch.uint8, device="cuda")
+    bad = C.c_int32(-1)
+    s = torch.cuda.current_stream().cuda_stream
+
+    def make8(r):
+        return np.rint(np.stack([cf.synth_image(h, w, seed=40 + 7 * r + p, n_rects=5, n_discs=5,
+                                                sigma=0.1) for p in range(P)]) * 255).astype(
+            np.uint8)
+
+    def run8(q):
+        q_d.copy_(torch.from_numpy(q))
+        rc = L.cf_wmc_filter_u8_u8(q_d.data_ptr(), w, h * w, o_d.data_ptr(), w, h * w, w, h, P,
+                                   iters, 1.0, ws8.data_ptr(), nb8, C.byref(bad), s)
+        assert rc == 0 and bad.value == 0
+        return (o_d.cpu().numpy(),)
+
+    _graph_cache_rounds(run8, make8, lambda q: (
+        oracle.quantize_u8(oracle.flow_f32(oracle.u8_to_f32(q), iters, 1.0)[0]),))
+
+    f_d, u_d, d_d = (torch.empty((P, h, w), device="cuda") for _ in range(3))
+    nb1 = int(L.cf_wmc_solve_l1_area_workspace_bytes(w, h, w, P, h * w))
+    ws1 = torch.empty(nb1, dtype=torch.uint8, device="cuda")
+    lam, alpha, dt = 2.5, 0.3, 0.2
+
+    def make1(r):
+        return np.stack([cf.synth_image(h, w, seed=60 + 7 * r + p, n_rects=5, n_discs=5,
+                                        sigma=0.1) for p in range(P)])
+
+    def run1(f):
+        f_d.copy_(torch.from_numpy(f))
+        rc = L.cf_wmc_solve_l1_area_f32(f_d.data_ptr(), u_d.data_ptr(), d_d.data_ptr(), w, h, w,
+                                        P, h * w, iters, dt, lam, alpha, 1, ws1.data_ptr(), nb1,
+                                        C.byref(bad), s)
+        assert rc == 0 and bad.value == 0
+        return u_d.cpu().numpy(), d_d.cpu().numpy()
+
+    _graph_cache_rounds(run1, make1, lambda f: oracle.solve_l1_area_f32(f, iters, dt, lam,
+                                                                       alpha)[:2])
+
+
+def test_graph_cache_inside_user_capture():
+    """A caller that captures the ABI call into its own graph gets the plain
+    launches (no nested graph); replaying the caller's graph stays exact."""
+    h, w, iters = 64, 300, 10
+    x = torch.empty((h, w), device="cuda")
+    ws = torch.empty(cf.workspace_bytes(h, w), dtype=torch.uint8, device="cuda")
+    cfg = cf.FlowConfig(iters=iters)
+    for _ in range(2):   # key seen twice outside capture: a cached graph exists too
+        cf.mc_flow(x.uniform_(), cfg, workspace=ws, inplace=True, check_finite=False)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            cf.mc_flow(x, cfg, workspace=ws, inplace=True, check_finite=False)
+    torch.cuda.current_stream().wait_stream(s)
+    for r in range(3):
+        a = cf.synth_image(h, w, seed=300 + r, n_rects=4, n_discs=4, sigma=0.1)
+        x.copy_(torch.from_numpy(a))
+        g.replay()
+        torch.cuda.synchronize()
+        assert_bitexact(x.cpu().numpy(), oracle.flow_f32(a, iters, 1.0)[0], f"user graph {r}")
