@@ -844,3 +844,56 @@ def test_graph_cache_inside_user_capture():
         g.replay()
         torch.cuda.synchronize()
         assert_bitexact(x.cpu().numpy(), oracle.flow_f32(a, iters, 1.0)[0], f"user graph {r}")
+
+
+def test_graph_cache_eviction_and_threads():
+    """More distinct calls than the cache holds (LRU eviction while graphs may
+    still be in flight), then host threads hitting the cache concurrently,
+    each with its own buffers and stream: every result bit-exact."""
+    import threading
+
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    h, w, iters = 33, 150, 4
+    img = cf.synth_image(h, w, seed=77, n_rects=4, n_discs=4, sigma=0.1)
+    nb = int(L.cf_wmc_filter_workspace_bytes(w, h, w, 1, h * w))
+    x = torch.empty((h, w), device="cuda")
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    dts = [0.25 + 0.015 * i for i in range(40)]          # 40 keys > 32 slots
+    refs = {dt: oracle.flow_f32(img, iters, dt)[0] for dt in dts}
+    s = torch.cuda.current_stream().cuda_stream
+    for rnd in range(3):                                  # direct, capture, replay / evicted
+        for dt in dts:
+            x.copy_(torch.from_numpy(img))
+            assert L.cf_wmc_filter_f32(x.data_ptr(), w, h, w, 1, h * w, iters, dt,
+                                       ws.data_ptr(), nb, None, s) == 0
+            torch.cuda.synchronize()
+            assert_bitexact(x.cpu().numpy(), refs[dt], f"round {rnd} dt={dt}")
+
+    errors = []
+
+    def worker(tid):
+        try:
+            stream = torch.cuda.Stream()
+            xt = torch.empty((h, w), device="cuda")
+            wt = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            dt = dts[tid]
+            for _ in range(6):
+                with torch.cuda.stream(stream):
+                    xt.copy_(torch.from_numpy(img))
+                    rc = L.cf_wmc_filter_f32(xt.data_ptr(), w, h, w, 1, h * w, iters, dt,
+                                             wt.data_ptr(), nb, None, stream.cuda_stream)
+                stream.synchronize()
+                if rc != 0:
+                    errors.append(f"thread {tid}: rc {rc}")
+                elif not np.array_equal(bits(xt.cpu().numpy()), bits(refs[dt])):
+                    errors.append(f"thread {tid}: mismatch")
+        except Exception as e:  # noqa: BLE001
+            errors.append(f"thread {tid}: {e!r}")
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
