@@ -480,40 +480,44 @@ def bench_b200(args, cfg):
         flag_off = (P * H * W * 4 + 255) // 256 * 256 if cfg.u8 else 0
         wss = [torch.empty(ws_e2e, dtype=torch.uint8, device=dev) for _ in range(NB)]
         ev_out = [torch.cuda.Event() for _ in range(NB)]
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_c = [torch.cuda.Event() for _ in range(NB)]
         for e in ev_out:
             e.record(s_out)
         flag_host = torch.zeros(NB, dtype=torch.int32).pin_memory()
         e2e_i = [0]
+        # copies through cf_copy (cudaMemcpyAsync on an explicit stream) and
+        # events created once: the host loop stays cheaper than the GPU step
+        # even for cfg1's ~10 us map
+        sp_in, sp_out = s_in.cuda_stream, s_out.cuda_stream
+        in_bytes = host_t.numel() * host_t.element_size()
+        out_bytes = out_host.numel() * out_host.element_size()
+        fcfg = cf.FlowConfig(dt=cfg.dt, iters=cfg.iters)
 
         def e2e_step():
             i = e2e_i[0]
             e2e_i[0] += 1
             b = i % NB
-            with torch.cuda.stream(s_in):
-                s_in.wait_event(ev_out[b])           # buffer b's previous D2H done
-                dbufs[b].copy_(host_t, non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(s_in)
-            stream.wait_event(ev_in)
+            s_in.wait_event(ev_out[b])               # buffer b's previous D2H done
+            assert L.cf_copy(dbufs[b].data_ptr(), host_t.data_ptr(), in_bytes, sp_in) == 0
+            ev_in[b].record(s_in)
+            stream.wait_event(ev_in[b])
             if cfg.iters == 0:
                 L.cf_wmc_map_f32(dbufs[b].data_ptr(), obufs[b].data_ptr(), W, H, W, P, H * W, sp)
                 res = obufs[b]
             elif cfg.u8:
-                res = cf.mc_flow_u8(dbufs[b], cf.FlowConfig(dt=cfg.dt, iters=cfg.iters),
-                                    workspace=wss[b], out=obufs[b], check_finite=False,
-                                    out_dtype="u8")
+                res = cf.mc_flow_u8(dbufs[b], fcfg, workspace=wss[b], out=obufs[b],
+                                    check_finite=False, out_dtype="u8")
             else:
-                res = cf.mc_flow(dbufs[b], cf.FlowConfig(dt=cfg.dt, iters=cfg.iters),
-                                 workspace=wss[b], inplace=True, check_finite=False)
+                res = cf.mc_flow(dbufs[b], fcfg, workspace=wss[b], inplace=True,
+                                 check_finite=False)
             if cfg.iters > 0:  # non-finite flag of this step (device check), read async
-                flag_host[b:b + 1].copy_(wss[b][flag_off:flag_off + 4].view(torch.int32),
-                                         non_blocking=True)
-            ev_c = torch.cuda.Event()
-            ev_c.record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_c)
-                out_host.copy_(res.reshape(out_host.shape), non_blocking=True)
-                ev_out[b].record(s_out)
+                assert L.cf_copy(flag_host[b:b + 1].data_ptr(), wss[b].data_ptr() + flag_off, 4,
+                                 sp) == 0
+            ev_c[b].record(stream)
+            s_out.wait_event(ev_c[b])
+            assert L.cf_copy(out_host.data_ptr(), res.data_ptr(), out_bytes, sp_out) == 0
+            ev_out[b].record(s_out)
     else:
         # row bands: the band runs in place in the flow's own buffers, so the
         # copies go through device staging buffers (2 each way): step i+1's
