@@ -280,8 +280,10 @@ uint32_t f32_bits(float v) {
     return b;
 }
 
-// Runs `enqueue` directly or through a cached graph.  Holds g_graph_mu while
-// capturing (once per key): the capture stream is shared per device.
+// Runs `enqueue` directly or through a cached graph.  g_graph_mu covers the
+// lookup, the capture (once per key: the capture stream is shared per device)
+// and cudaGraphLaunch (an exec must not be evicted mid-launch); a key's
+// first, plain run happens outside it.
 template <typename Fn>
 int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
     if (!graphs_enabled()) return enqueue(s);
@@ -291,7 +293,7 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
         return enqueue(s);
     }
     if (cs != cudaStreamCaptureStatusNone) return enqueue(s);
-    std::lock_guard<std::mutex> lk(g_graph_mu);
+    std::unique_lock<std::mutex> lk(g_graph_mu);
     const uint64_t now = ++g_graph_clock;
     GraphEntry* hit = nullptr;
     for (GraphEntry& e : g_graphs)
@@ -309,6 +311,7 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
         e.key = key;
         e.last_use = now;
         g_graphs.push_back(e);
+        lk.unlock();  // plain launches need no lock (other threads keep going)
         return enqueue(s);
     }
     hit->last_use = now;
