@@ -220,14 +220,78 @@ std::vector<int> schedule(int iters, int levels) {
 __global__ void u8_to_f32_kernel(const uint8_t* in, int64_t in_pitch, int64_t in_plane, float* out,
                                  int64_t pitch, int64_t plane, int32_t w, int32_t h,
                                  int32_t planes) {
-    // one row per block iteration: a single index division per row
+    // one row per block iteration (a single index division per row); rows
+    // whose source is 4-byte and destination 16-byte aligned move 4 pixels
+    // per thread (one 32-bit load, one 128-bit store), others 1
     const int64_t rows = (int64_t)h * planes;
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const int64_t p = r / h, y = r - p * h;
         const uint8_t* src = in + p * in_plane + y * in_pitch;
         float* dst = out + p * plane + y * pitch;
-        for (int x = threadIdx.x; x < w; x += blockDim.x) dst[x] = __fdiv_rn((float)src[x], 255.0f);
+        int x0 = 0;
+        if ((reinterpret_cast<uintptr_t>(src) & 3) == 0 &&
+            (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            const int n4 = w >> 2;
+            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+            float4* d4 = reinterpret_cast<float4*>(dst);
+            for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+                const uint32_t v = __ldg(s4 + i);
+                d4[i] = make_float4(cfk::widen_u8(v & 0xffu), cfk::widen_u8((v >> 8) & 0xffu),
+                                    cfk::widen_u8((v >> 16) & 0xffu), cfk::widen_u8(v >> 24));
+            }
+            x0 = n4 << 2;
+        }
+        for (int x = x0 + threadIdx.x; x < w; x += blockDim.x) dst[x] = cfk::widen_u8(src[x]);
     }
+}
+
+__device__ __forceinline__ float4 widen4(uint32_t v) {
+    return make_float4(cfk::widen_u8(v & 0xffu), cfk::widen_u8((v >> 8) & 0xffu),
+                       cfk::widen_u8((v >> 16) & 0xffu), cfk::widen_u8(v >> 24));
+}
+
+__global__ void u8_to_f32_dense_kernel(const uint32_t* in, float4* out, int64_t n4) {
+    // dense planes (pitch w, plane stride h*w): the batch is one flat array
+    // of 4-pixel words.  Consecutive threads take consecutive words, so every
+    // warp load is 128 contiguous bytes and every float4 store 512; four
+    // words per thread (grid-stride apart) are loaded before any is stored.
+    const int64_t S = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * S < n4; i += 4 * S) {
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldg(in + i + k * S);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[i + k * S] = widen4(v[k]);
+    }
+    for (; i < n4; i += S) out[i] = widen4(__ldg(in + i));
+}
+
+// u8 -> fp32 widening of a plane batch, flat when dense.
+int launch_widen(const uint8_t* in, int64_t in_pitch, int64_t in_plane, float* out, int64_t pitch,
+                 int64_t plane, int32_t w, int32_t h, int32_t planes, int sms, cudaStream_t s) {
+    const int64_t hw = (int64_t)h * w, n = hw * planes;
+    const bool dense = in_pitch == w && pitch == w && (planes == 1 || (in_plane == hw && plane == hw));
+    if (dense && (reinterpret_cast<uintptr_t>(in) & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(out) & 15) == 0 && n >= 4) {
+        const int64_t n4 = n / 4;
+        const int64_t blocks = std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8);
+        u8_to_f32_dense_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+            reinterpret_cast<const uint32_t*>(in), reinterpret_cast<float4*>(out), n4);
+        CF_CUDA(cudaGetLastError());
+        if (n4 * 4 == n) return CF_OK;
+        // tail (< 4 pixels, contiguous: may span rows when w < 4): one
+        // "row" of n - done pixels through the row kernel
+        const int64_t done = n4 * 4;
+        u8_to_f32_kernel<<<1, 256, 0, s>>>(in + done, 0, 0, out + done, 0, 0,
+                                           (int32_t)(n - done), 1, 1);
+        CF_CUDA(cudaGetLastError());
+        return CF_OK;
+    }
+    u8_to_f32_kernel<<<sms * 16, 256, 0, s>>>(in, in_pitch, in_plane, out, pitch, plane, w, h,
+                                           planes);
+    CF_CUDA(cudaGetLastError());
+    return CF_OK;
 }
 
 // ---- launch-graph cache -----------------------------------------------------
@@ -461,9 +525,9 @@ static int enqueue_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_
         // widen u8 -> fp32 into whichever buffer makes the
         // final launch land in `out`
         if (ks.size() % 2 == 1) std::swap(cur, nxt);
-        u8_to_f32_kernel<<<148 * 16, 256, 0, s>>>(static_cast<const uint8_t*>(src0), src_pitch,
-                                               src_plane, cur, pitch, plane_stride, w, h, planes);
-        CF_CUDA(cudaGetLastError());
+        if (int rc = launch_widen(static_cast<const uint8_t*>(src0), src_pitch, src_plane, cur,
+                                  pitch, plane_stride, w, h, planes, d.sms, s))
+            return rc;
     }
     int iter = 0;
     for (size_t i = 0; i < ks.size(); ++i) {
@@ -564,10 +628,10 @@ CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_
     if (first_bad_iter) *first_bad_iter = 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (iters == 0) {
-        u8_to_f32_kernel<<<148 * 16, 256, 0, s>>>(in, in_pitch, in_plane_stride, out, pitch,
-                                               plane_stride, w, h, planes);
-        CF_CUDA(cudaGetLastError());
-        return CF_OK;
+        DevInfo d;
+        if (int rc = device_info(&d)) return rc;
+        return launch_widen(in, in_pitch, in_plane_stride, out, pitch, plane_stride, w, h, planes,
+                            d.sms, s);
     }
     if (!workspace ||
         workspace_bytes < cf_wmc_filter_workspace_bytes(w, h, pitch, planes, plane_stride))

@@ -135,6 +135,18 @@ __device__ __forceinline__ uint8_t quantize_u8(float v) {
     return (uint8_t)__float2int_rn(__fmul_rn(c, 255.0f));
 }
 
+// Load-time widening: fl(q / 255) for a byte q, without the
+// division.  r0 = fl(q * fl(1/255)) is off by one ulp for 126 of the 256
+// bytes; one residual step r = fma(fma(-r0, 255, q), fl(1/255), r0) equals
+// the IEEE quotient for all 256 (checked exhaustively with exact rationals,
+// and bit-compared against __fdiv_rn in tests/test_gpu_parity.py).
+__device__ __forceinline__ float widen_u8(uint32_t q) {
+    const float qf = __uint2float_rn(q);
+    const float inv = 0x1.010102p-8f;  // fl(1/255)
+    const float r0 = __fmul_rn(qf, inv);
+    return __fmaf_rn(__fmaf_rn(-r0, 255.0f, qf), inv, r0);
+}
+
 constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_flow)
 constexpr int kModeMap = 1;   // out = H^w(U), one level, fp64 near-tie rule (wmc_half_laplace)
 constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)

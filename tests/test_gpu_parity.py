@@ -897,3 +897,35 @@ def test_graph_cache_eviction_and_threads():
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("P,h,w,in_pitch,out_pitch,src_off", [
+    (4, 64, 256, 256, 256, 0),      # dense, 16-byte aligned: flat kernel, no tail
+    (3, 7, 5, 5, 5, 0),             # dense, 105 px: flat + a 9-px tail spanning rows
+    (2, 10, 3, 3, 3, 0),            # w < 16: tail of 12 px over 4 rows
+    (2, 33, 101, 104, 104, 0),      # pitched: row kernel, 4-aligned source rows
+    (2, 33, 101, 101, 104, 0),      # odd source pitch: scalar rows
+    (1, 40, 256, 256, 256, 1),      # dense but misaligned source: row kernel
+    (256, 9, 32, 32, 32, 0),        # many planes (cfg5-like batch)
+])
+def test_widen_u8_all_bytes_every_path(P, h, w, in_pitch, out_pitch, src_off):
+    """u8 -> fp32 load widening without a division: every byte
+    value through every kernel path equals the IEEE quotient q / 255."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    rng = np.random.default_rng(P * 1000 + w)
+    q = rng.integers(0, 256, size=(P, h, w), dtype=np.uint8)
+    q.reshape(-1)[:256] = np.arange(256, dtype=np.uint8)[:min(256, q.size)]
+    src = np.zeros((P, h, in_pitch), dtype=np.uint8)
+    src[:, :, :w] = q
+    flat = torch.zeros(src.size + 16, dtype=torch.uint8, device="cuda")
+    flat[src_off:src_off + src.size] = torch.from_numpy(src.reshape(-1)).cuda()
+    out = torch.full((P, h, out_pitch), -1.0, device="cuda")
+    rc = L.cf_wmc_filter_u8_f32(flat.data_ptr() + src_off, in_pitch, h * in_pitch, out.data_ptr(),
+                                w, h, out_pitch, P, h * out_pitch, 0, 1.0, None, 0, None,
+                                torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    got = out.cpu().numpy()
+    ref = (q.astype(np.float32) / np.float32(255)).astype(np.float32)
+    assert_bitexact(got[:, :, :w], ref, "widen")
+    assert np.all(got[:, :, w:] == -1.0)       # pitch padding untouched
