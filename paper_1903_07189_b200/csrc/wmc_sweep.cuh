@@ -130,9 +130,10 @@ struct SweepParams {
 
 // Per-pixel update a launch applies at every level.
 // Save-time quantisation, shared with csrc/wmc_io.cu.
-__device__ __forceinline__ uint8_t quantize_u8(float v) {
-    const float c = fminf(fmaxf(v, 0.0f), 1.0f);  // NaN -> 0 (fmaxf returns the number)
-    return (uint8_t)__float2int_rn(__fmul_rn(c, 255.0f));
+__device__ __forceinline__ uint32_t quantize_u8(float v) {
+    // clamp(v, 0, 1) as one saturating op: NaN -> +0 (the clamp's fmaxf also
+    // gives 0; +-0 both quantise to byte 0), then rint(c * 255)
+    return (uint32_t)__float2int_rn(__fmul_rn(__saturatef(v), 255.0f));
 }
 
 // Load-time widening: fl(q / 255) for a byte q, without the
@@ -396,6 +397,7 @@ struct SweepWarp {
     bool outc[C];                 // column j of this lane is an output column
     bool out_h[2];                // chunk h exists (a missing chunk is never stored)
     bool border;                  // some window touches column 0 or w-1 (uniform)
+    bool st16;                    // kModeFlowU8: even output rows (16-bit byte-pair stores)
     uint32_t emask;               // image-edge columns of this lane (edge_fix)
     int ys, ye;                   // output strip rows
     // rows computed per level L: [rlo(L), rhi(L)) (recomputed, not stored)
@@ -637,13 +639,27 @@ struct SweepWarp {
         if constexpr (L < K) store<L + 1, CHECKED, EDGE>(t, R4, sptr);
     }
 
-    // This lane's output columns of a level-K row as quantised bytes.
+    // This lane's output columns of a level-K row as quantised bytes.  FAST
+    // (interior warp, unchecked step) with K even: a lane's C = 2 columns
+    // start at an even column (chunk origin chunk*S - K) and are both output
+    // or both halo, so each chunk's pair is one aligned 16-bit store.
+    template <bool FAST>
     __device__ __forceinline__ void store_row8(uint8_t* row, const f2 (&nv)[C]) const {
+        if constexpr (FAST && C == 2 && (G::A & 1) == 0) {
+            if (!outc[0]) return;
+            if (st16) {  // even row addresses (base and pitch)
+                const uint32_t b0 = quantize_u8(lo(nv[0])) | (quantize_u8(lo(nv[1])) << 8);
+                const uint32_t b1 = quantize_u8(hi(nv[0])) | (quantize_u8(hi(nv[1])) << 8);
+                *reinterpret_cast<uint16_t*>(row + xf[0]) = (uint16_t)b0;
+                *reinterpret_cast<uint16_t*>(row + xf[1]) = (uint16_t)b1;
+                return;
+            }
+        }
 #pragma unroll
         for (int j = 0; j < C; ++j) {
             if (!outc[j]) continue;
-            if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = quantize_u8(lo(nv[j]));
-            if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = quantize_u8(hi(nv[j]));
+            if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = (uint8_t)quantize_u8(lo(nv[j]));
+            if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = (uint8_t)quantize_u8(hi(nv[j]));
         }
     }
 
@@ -674,7 +690,7 @@ struct SweepWarp {
             }
         }
         if constexpr (L == K && MODE == kModeFlowU8) {  // quantise in the store
-            store_row8(d8p + (int64_t)(y - P.dst_row0) * P.dst8_pitch, nv);
+            store_row8<!(CHECKED || EDGE)>(d8p + (int64_t)(y - P.dst_row0) * P.dst8_pitch, nv);
             return;
         }
         if constexpr (L == K) {
@@ -944,6 +960,7 @@ __global__ void __launch_bounds__(kThreads,
     sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
     sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
     sw.d8p = MODE == kModeFlowU8 ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
+    sw.st16 = ((reinterpret_cast<uintptr_t>(sw.d8p) | (uintptr_t)p.dst8_pitch) & 1) == 0;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K, MODE>();
     sw.lbase = sw.sbase + 8 * C * sw.lane;

@@ -929,3 +929,31 @@ def test_widen_u8_all_bytes_every_path(P, h, w, in_pitch, out_pitch, src_off):
     ref = (q.astype(np.float32) / np.float32(255)).astype(np.float32)
     assert_bitexact(got[:, :, :w], ref, "widen")
     assert np.all(got[:, :, w:] == -1.0)       # pitch padding untouched
+
+
+@pytest.mark.parametrize("out_pitch,out_off", [(640, 0), (641, 0), (640, 1), (643, 3)])
+def test_u8_out_store_alignment(out_pitch, out_off):
+    """Fused u8 quantisation (kModeFlowU8): 16-bit byte-pair stores when the
+    output rows are even, byte stores otherwise -- same bytes either way."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    P, h, w, iters = 2, 70, 620, 6
+    q = np.rint(np.stack([cf.synth_image(h, w, seed=500 + p, n_rects=6, n_discs=6, sigma=0.1)
+                          for p in range(P)]) * 255).astype(np.uint8)
+    qd = torch.from_numpy(q).cuda()
+    plane = h * out_pitch + 5
+    buf = torch.full((P * plane + out_off + 16,), 7, dtype=torch.uint8, device="cuda")
+    nb = int(L.cf_wmc_filter_u8_u8_workspace_bytes(w, h, P))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    rc = L.cf_wmc_filter_u8_u8(qd.data_ptr(), w, h * w, buf.data_ptr() + out_off, out_pitch, plane,
+                               w, h, P, iters, 1.0, ws.data_ptr(), nb, None,
+                               torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    flat = buf.cpu().numpy()
+    ref = oracle.quantize_u8(oracle.flow_f32(oracle.u8_to_f32(q), iters, 1.0)[0])
+    for p in range(P):
+        base = out_off + p * plane
+        got = flat[base:base + h * out_pitch].reshape(h, out_pitch)
+        assert np.array_equal(got[:, :w], ref[p]), f"plane {p}"
+        assert np.all(got[:, w:] == 7)           # pitch padding untouched
+    assert np.all(flat[:out_off] == 7)
