@@ -679,12 +679,18 @@ def bench_reference(args, cfg):
                 oracle.wmc_map_f64(img, threads)
         else:
             oracle.flow_f64(img, n, cfg.dt, threads)
-    # a step = n iterations (map evaluations) on the crop, n sized to ~0.5 s
+    # a step = n iterations (map evaluations) on the crop, n sized to ~2 s
+    # from the MARGINAL cost of an iteration (run(2) - run(1)): each call
+    # allocates and first-touches its fp64 buffers (~0.15 s on a 2048^2 crop),
+    # which a 10-iteration step would report as half the reference's time
     run(1)
     t0 = time.perf_counter()
     run(1)
-    one = max(time.perf_counter() - t0, 1e-6)
-    n_it = max(1, min(cfg.iters or 50, int(0.5 / one)))
+    t1 = time.perf_counter()
+    run(2)
+    t2 = time.perf_counter()
+    one = max((t2 - t1) - (t1 - t0), (t1 - t0) / 4, 1e-6)
+    n_it = max(1, min(cfg.iters or 50, int(2.0 / one)))
 
     def sample():
         run(n_it)
