@@ -27,6 +27,11 @@
  *  - Returns CF_OK (0) or a status below; no exceptions cross the ABI.
  *    CF_ECUDA keeps the CUDA error in thread-local state (cf_last_cuda_error).
  *  - Re-entrant: concurrent calls on different streams are safe.
+ *  - The filter / solver entry points keep a small LRU of CUDA graphs keyed
+ *    on all of their arguments.  From the second identical call on, the
+ *    launch chain replays as one graph on `stream`: same results, no
+ *    per-launch gaps.  Calls made while `stream` is capturing launch
+ *    directly.  Environment CF_GRAPHS=0 disables the cache.
  *  - Results are bit-identical for every launch configuration, temporal
  *    depth and band decomposition, and equal to the canonical fp32
  *    evaluation documented in DESIGN.md §3 (oracle/wmc_oracle.c).
