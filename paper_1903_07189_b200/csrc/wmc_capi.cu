@@ -321,6 +321,7 @@ struct FlowKey {
 struct GraphEntry {
     FlowKey key;
     cudaGraphExec_t exec = nullptr;  // null: seen once, not captured yet
+    bool no_graph = false;           // capture failed once: plain launches for this key
     uint64_t last_use = 0;
 };
 
@@ -379,6 +380,10 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
         return enqueue(s);
     }
     hit->last_use = now;
+    if (hit->no_graph) {
+        lk.unlock();
+        return enqueue(s);
+    }
     if (!hit->exec) {  // second sighting: capture on the device's capture stream
         if ((int)g_capture_streams.size() <= key.dev) g_capture_streams.resize(key.dev + 1, nullptr);
         cudaStream_t& cap = g_capture_streams[key.dev];
@@ -387,16 +392,14 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
         const int rc = enqueue(cap);
         cudaGraph_t g = nullptr;
         const cudaError_t ec = cudaStreamEndCapture(cap, &g);
-        if (rc || ec != cudaSuccess) {
-            if (g) cudaGraphDestroy(g);
+        cudaError_t ei = cudaErrorUnknown;
+        if (!rc && ec == cudaSuccess) ei = cudaGraphInstantiate(&hit->exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (ei != cudaSuccess) {  // capture refused: plain launches from now on (a
+            hit->exec = nullptr;  // genuine argument error recurs there and is returned)
+            hit->no_graph = true;
             (void)cudaGetLastError();
-            return rc ? rc : enqueue(s);  // capture refused: plain launches
-        }
-        const cudaError_t ei = cudaGraphInstantiate(&hit->exec, g, 0);
-        cudaGraphDestroy(g);
-        if (ei != cudaSuccess) {
-            hit->exec = nullptr;
-            (void)cudaGetLastError();
+            lk.unlock();
             return enqueue(s);
         }
     }
