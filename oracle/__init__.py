@@ -55,6 +55,22 @@ def lib():
         L.or_histogram_from_map.argtypes = [_vp, _i64, _f32, _f32, _f32, _i32, _vp]
         L.or_histogram_from_map.restype = None
         L.or_wmc_naive_f64.argtypes = [_vp, _vp, _i32, _i32]
+        L.or_synth_f32.argtypes = [_vp, _i32, _i32, _i64, C.c_uint64, _i32, _i32, _f64, _i32]
+        L.or_synth_f32.restype = C.c_int
+        L.or_synth_u8.argtypes = [_vp, _i32, _i32, _i64, C.c_uint64, _i32, _i32, _f64, _i32]
+        L.or_synth_u8.restype = C.c_int
+        L.or_fast_supported.argtypes = []
+        L.or_fast_supported.restype = C.c_int
+        L.or_fast_w64_matches.argtypes = []
+        L.or_fast_w64_matches.restype = C.c_int
+        L.or_fast_flow_f32.argtypes = [_vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32, _i32, _pi32]
+        L.or_fast_flow_f32.restype = C.c_int
+        L.or_fast_map_f32.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _i32, _vp]
+        L.or_fast_map_f32.restype = C.c_int
+        L.or_fast_flow_f64.argtypes = [_vp, _i32, _i32, _i32, _f64, _i32, _pi32]
+        L.or_fast_flow_f64.restype = C.c_int
+        L.or_fast_map_f64.argtypes = [_vp, _vp, _i32, _i32, _i32]
+        L.or_fast_map_f64.restype = C.c_int
         L.or_kernel_bank_numerators.argtypes = [_pi32]
         for f in ("or_wmc_map_f64", "or_wmc_map_f32", "or_flow_f32", "or_flow_f64"):
             getattr(L, f).restype = C.c_int
@@ -274,3 +290,95 @@ def wmc_histogram(img, scale=255.0, lo=-256.0, width=1.0, nbins=512, threads=Non
     lib().or_histogram_from_map(m.ctypes.data, m.size, float(scale), float(lo), float(width),
                                 int(nbins), counts.ctypes.data)
     return counts
+
+
+# ---------------------------------------------------------------------------
+# Vectorised restatements (oracle/wmc_fast.c): the same sequences, bit-identical
+# to the scalar functions above (tests/test_oracle_fast.py), fast enough for the
+# full BASELINE configurations.  On a CPU without AVX2/FMA they run the scalar
+# functions instead.
+
+def fast_supported() -> bool:
+    return bool(lib().or_fast_supported())
+
+
+def flow_f32_fast(img, iters, dt=1.0, threads=None, inplace=False):
+    """flow_f32, vectorised; img (H, W) or (P, H, W) float32.  inplace=True
+    filters a C-contiguous float32 array in place (no copy of big inputs)."""
+    if not fast_supported():
+        return flow_f32(img, iters, dt, threads)
+    if inplace:
+        a = img
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    else:
+        a = np.array(img, dtype=np.float32, order="C", copy=True)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    bad = C.c_int32(0)
+    rc = lib().or_fast_flow_f32(a3.ctypes.data, w, h, w, P, h * w, int(iters), float(dt),
+                                _threads(threads), C.byref(bad))
+    assert rc in (0, 3), rc
+    return (a3[0] if a.ndim == 2 else a3), bad.value
+
+
+def wmc_map_f32_fast(img, threads=None, return_ties=False):
+    """wmc_map_f32 (tie rule included), vectorised."""
+    if not fast_supported():
+        return wmc_map_f32(img, threads, return_ties)
+    a = np.ascontiguousarray(img, dtype=np.float32)
+    a3 = a[None] if a.ndim == 2 else a
+    P, h, w = a3.shape
+    out = np.empty_like(a3)
+    ties = np.zeros(a3.shape, dtype=np.int8) if return_ties else None
+    rc = lib().or_fast_map_f32(a3.ctypes.data, out.ctypes.data, w, h, w, P, h * w,
+                               _threads(threads), ties.ctypes.data if ties is not None else None)
+    assert rc == 0
+    res = out[0] if a.ndim == 2 else out
+    if return_ties:
+        return res, (ties[0] if a.ndim == 2 else ties)
+    return res
+
+
+def flow_f64_fast(img, iters, dt=1.0, threads=None):
+    """flow_f64 (SPEC-faithful fp64), vectorised; img (H, W)."""
+    if not fast_supported():
+        return flow_f64(img, iters, dt, threads)
+    a = np.array(img, dtype=np.float64, order="C", copy=True)
+    h, w = a.shape
+    bad = C.c_int32(0)
+    rc = lib().or_fast_flow_f64(a.ctypes.data, w, h, int(iters), float(dt), _threads(threads),
+                                C.byref(bad))
+    assert rc in (0, 3), rc
+    return a, bad.value
+
+
+def wmc_map_f64_fast(img, threads=None):
+    """wmc_map_f64 (SPEC-faithful fp64), vectorised; img (H, W)."""
+    if not fast_supported():
+        return wmc_map_f64(img, threads)
+    a = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = a.shape
+    out = np.empty_like(a)
+    assert lib().or_fast_map_f64(a.ctypes.data, out.ctypes.data, w, h, _threads(threads)) == 0
+    return out
+
+
+def synth(w, h, seed, n_rects, n_discs, sigma, u8=False, threads=None):
+    """The seeded synthetic image from oracle/synth_ref.c --
+    byte-identical to the product's cf_synth_f32 / cf_synth_u8, without
+    loading the product library (bench.py's CPU legs)."""
+    out = np.empty((h, w), dtype=np.uint8 if u8 else np.float32)
+    fn = lib().or_synth_u8 if u8 else lib().or_synth_f32
+    rc = fn(out.ctypes.data, int(w), int(h), int(w), int(seed) & (2**64 - 1), int(n_rects),
+            int(n_discs), float(sigma), _threads(threads))
+    assert rc == 0
+    return out
+
+
+def synth_config(cfg, planes=None, threads=None):
+    """Input of a BASELINE config (paper_1903_07189_b200/configs.py WmcConfig):
+    (H, W) for one plane, else (P, H, W); u8 configs give uint8."""
+    n = cfg.planes if planes is None else planes
+    imgs = [synth(cfg.w, cfg.h, cfg.seed(p), cfg.n_rects, cfg.n_discs, cfg.sigma, cfg.u8,
+                  threads) for p in range(n)]
+    return imgs[0] if n == 1 and planes is None else np.stack(imgs)

@@ -65,6 +65,13 @@
 
 OR_EXPORT void or_kernel_bank_numerators(int32_t* out72) { kernel_bank_numerators(out72); }
 
+/* 1 when this CPU can run wmc_fast.c (built with -mavx2 -mfma); the Python
+ * wrapper falls back to the scalar functions here otherwise. */
+OR_EXPORT int or_fast_supported(void) {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+}
+
 /* ------------------------------------------------------------------------ */
 /* for_rows restatement (parallel.hpp:26-47)                                 */
 /* ------------------------------------------------------------------------ */

@@ -387,23 +387,34 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
     if (!hit->exec) {  // second sighting: capture on the device's capture stream
         if ((int)g_capture_streams.size() <= key.dev) g_capture_streams.resize(key.dev + 1, nullptr);
         cudaStream_t& cap = g_capture_streams[key.dev];
-        if (!cap) CF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-        CF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-        const int rc = enqueue(cap);
-        cudaGraph_t g = nullptr;
-        const cudaError_t ec = cudaStreamEndCapture(cap, &g);
-        cudaError_t ei = cudaErrorUnknown;
-        if (!rc && ec == cudaSuccess) ei = cudaGraphInstantiate(&hit->exec, g, 0);
-        if (g) cudaGraphDestroy(g);
-        if (ei != cudaSuccess) {  // capture refused: plain launches from now on (a
-            hit->exec = nullptr;  // genuine argument error recurs there and is returned)
+        bool ok = cap || cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess;
+        if (ok && cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const int rc = enqueue(cap);
+            cudaGraph_t g = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(cap, &g);
+            ok = !rc && ec == cudaSuccess && g &&
+                 cudaGraphInstantiate(&hit->exec, g, 0) == cudaSuccess;
+            if (g) cudaGraphDestroy(g);
+        } else {
+            ok = false;
+        }
+        if (!ok) {  // capture refused or failed: plain launches for this key from now
+            hit->exec = nullptr;  // on (a genuine argument error recurs there and is returned)
             hit->no_graph = true;
             (void)cudaGetLastError();
             lk.unlock();
             return enqueue(s);
         }
     }
-    CF_CUDA(cudaGraphLaunch(hit->exec, s));
+    if (cudaGraphLaunch(hit->exec, s) != cudaSuccess) {
+        // e.g. the exec was invalidated (device reset): drop it, run plain launches
+        (void)cudaGetLastError();
+        cudaGraphExecDestroy(hit->exec);
+        hit->exec = nullptr;
+        hit->no_graph = true;
+        lk.unlock();
+        return enqueue(s);
+    }
     return CF_OK;
 }
 

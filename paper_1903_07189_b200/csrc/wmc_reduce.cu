@@ -143,6 +143,7 @@ CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pit
                              void* workspace, size_t workspace_bytes, void* stream) {
     if (!img || !d_out || !workspace || w <= 0 || h <= 0 || planes <= 0 || pitch < w)
         return CF_EINVAL;
+    if (planes > 1 && plane_stride < pitch * (int64_t)h) return CF_EINVAL;
     if (!(q > 0.0) || !(q < 1e300)) return CF_EINVAL;
     if (workspace_bytes < cf_wmc_reduce_workspace_bytes(w, h, planes)) return CF_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
@@ -186,6 +187,7 @@ CF_API int cf_wmc_histogram(const float* img, int32_t w, int32_t h, int64_t pitc
                             size_t workspace_bytes, void* stream) {
     if (!img || !d_counts || !workspace || w <= 0 || h <= 0 || planes <= 0 || pitch < w)
         return CF_EINVAL;
+    if (planes > 1 && plane_stride < pitch * (int64_t)h) return CF_EINVAL;
     if (nbins <= 0 || !(width > 0.0f) || !(scale == scale) || !(lo == lo)) return CF_EINVAL;
     if (workspace_bytes < cf_wmc_reduce_workspace_bytes(w, h, planes)) return CF_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;

@@ -128,8 +128,8 @@ struct SweepParams {
     float neg_inv_alpha;      // -fl(1/alpha)
 };
 
-// Per-pixel update a launch applies at every level.
-// Save-time quantisation, shared with csrc/wmc_io.cu.
+// Save-time quantisation of the fused u8 stores; wmc_io.cu's
+// quantize() is the same clamp-then-round (fminf/fmaxf form, equal bytes).
 __device__ __forceinline__ uint32_t quantize_u8(float v) {
     // clamp(v, 0, 1) as one saturating op: NaN -> +0 (the clamp's fmaxf also
     // gives 0; +-0 both quantise to byte 0), then rint(c * 255)

@@ -7,7 +7,12 @@ import paper_1903_07189_b200 as cf
 what = sys.argv[1] if len(sys.argv) > 1 else "map"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 H = W = 16384
-x = torch.rand((H, W), device="cuda")
+if what == "map":  # the supplemental map config's synthetic image (cfg1 generator)
+    from paper_1903_07189_b200.configs import SUPPLEMENTAL
+    c = SUPPLEMENTAL["cfg1_16k"]
+    x = torch.from_numpy(cf.synth_image(H, W, c.seed(0), c.n_rects, c.n_discs, c.sigma)).cuda()
+else:
+    x = torch.rand((H, W), device="cuda")
 y = torch.empty_like(x)
 s = torch.cuda.current_stream().cuda_stream
 for _ in range(n):
