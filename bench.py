@@ -37,6 +37,20 @@ BYTES_PER_UPDATE = 8  # 4 B read of U^t + 4 B write of U^{t+1}
 L2_BYTES = 126 * 1024 * 1024
 
 
+def _ncu_json():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def ncu_launch_ms(kernel: str, h: int, w: int, planes: int):
+    """ncu gpu__time_duration of one launch at this geometry (cold cache,
+    serialised) from the committed capture, else None."""
+    return _ncu_json().get(f"{kernel}@{planes}x{h}x{w}:ms")
+
+
 def ncu_traffic(kernel: str, h: int, w: int, planes: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at
     this geometry, from the committed ncu --set full capture
@@ -141,55 +155,86 @@ def make_input(cfg, rows=None, threads=0, planes=None):
     return np.stack(imgs) if cfg.planes > 1 else imgs[0]
 
 
-def marginal_cost(fn):
-    """(seconds per iteration, fixed seconds per call) of fn(n): the best of
-    two (fn(1), fn(4)) pairs after a warm call, so one slow early call
-    (page-in, a busy core) cannot shrink the sample."""
-    fn(1)
-    per, fixed = float("inf"), 0.0
-    for _ in range(2):
-        t0 = time.perf_counter()
-        fn(1)
-        t1 = time.perf_counter()
-        fn(4)
-        t2 = time.perf_counter()
-        p = max(((t2 - t1) - (t1 - t0)) / 3, (t1 - t0) / 8, 1e-6)
-        if p < per:
-            per, fixed = p, max(0.0, (t1 - t0) - p)
-    return per, fixed
+def load_configs():
+    """paper_1903_07189_b200/configs.py loaded as a standalone module, so the
+    reference arm imports nothing else from the product package."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_1903_07189_b200", "configs.py")
+    spec = importlib.util.spec_from_file_location("cf_bench_configs", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["cf_bench_configs"] = mod  # dataclasses resolve the module by name
+    spec.loader.exec_module(mod)
+    return mod.CONFIGS, mod.SUPPLEMENTAL
 
 
-def cpu_reference_sample(cfg, full, target_s=10.0):
-    """Time the reference CPU path (fp64 SPEC-faithful mc_flow / map, all host
-    threads) on a bounded crop of the workload's input `full` (plane 0).
-    Returns (Gupd/s, cores, sample description, kind)."""
-    import numpy as np
+def bench_config(cfg) -> dict:
+    """The workload's `config` object -- identical in both arms' JSON lines
+    (implementation details go to "impl_config")."""
+    return {"workload": workload_name(cfg), "iters": cfg.iters, "planes": cfg.planes,
+            "h": cfg.h, "w": cfg.w, "dt": cfg.dt}
 
-    import oracle
-    threads = os.cpu_count() or 1
-    crop_h = min(cfg.h, 2048)
-    crop_w = min(cfg.w, 2048)
-    img = np.ascontiguousarray(full[:crop_h, :crop_w], dtype=np.float64)
-    if cfg.u8:
-        img = img / 255.0
+
+def algorithmic_bytes(cfg, pixels: int, u8_out: bool) -> int:
+    """SURVEY.md §8d: 4 B read of U^t + 4 B write of U^{t+1} per pixel-update;
+    the u8 path reads 1 B on the first sweep and (u8 out) writes 1 B on the
+    last one.  `pixels` = pixels of one full-image pass."""
     if cfg.iters == 0:
-        fn = lambda n: [oracle.wmc_map_f64(img, threads) for _ in range(n)]  # noqa: E731
-    else:
-        fn = lambda n: oracle.flow_f64(img, n, cfg.dt, threads)  # noqa: E731
-    per, fixed = marginal_cost(fn)
-    # n iterations per call (at most the workload's), repeated like
-    # consecutive frames until ~target_s of CPU work
-    n = max(1, min(cfg.iters if cfg.iters else 50, int(target_s / per)))
-    reps = max(1, int(round(target_s / (n * per + fixed))))
+        return pixels * BYTES_PER_UPDATE
+    if not cfg.u8:
+        return pixels * cfg.iters * BYTES_PER_UPDATE
+    last_w = 1 if u8_out else 4
+    if cfg.iters == 1:
+        return pixels * (1 + last_w)
+    return pixels * ((1 + 4) + (cfg.iters - 2) * 8 + (4 + last_w))
+
+
+def cpu_reference(threads: int):
+    """The reference CPU path: the fp64 SPEC-faithful mc_flow / wmc_half_laplace
+    run on the reference's own executor (oracle/_ref/libcf_ref.so, compiled
+    against /root/reference/proj/include/curveflow/parallel.hpp:26-47), or,
+    when that build is absent, the oracle's for_rows restatement.
+    Returns (flow(img, n), map(img), kind, what)."""
+    import oracle
+    if oracle.ref_lib() is not None:
+        return (lambda img, n, dt: oracle.ref_flow_f64(img, n, dt, threads, inplace=True),
+                lambda img: oracle.ref_wmc_map_f64(img, threads), "reference",
+                "oracle/_ref/libcf_ref.so: the fp64 SPEC-faithful restatement on the "
+                "reference's own curveflow::parallel executor (parallel.hpp:26-47)")
+    return (lambda img, n, dt: oracle.flow_f64(img, n, dt, threads, inplace=True),
+            lambda img: oracle.wmc_map_f64(img, threads), "port",
+            "oracle/wmc_oracle.c: the fp64 SPEC-faithful restatement (for_rows port)")
+
+
+def cpu_reference_sample(cfg, img64, budget_s=10.0):
+    """Time the reference CPU path on a bounded sample of the workload: the
+    FULL-SIZE first plane `img64` (fp64, widened from u8 if needed), n of the
+    workload's iterations (a map workload: n evaluations), n sized from one
+    timed iteration so the sample is ~budget_s of CPU work.
+    Returns (Gupd/s, cores, sample description, kind, n, seconds per sample)."""
+    threads = os.cpu_count() or 1
+    flow, wmap, kind, what = cpu_reference(threads)
+    h, w = img64.shape
+    work = img64.copy()
     t0 = time.perf_counter()
-    for _ in range(reps):
-        fn(n)
-    dt = time.perf_counter() - t0
-    rate = crop_h * crop_w * n * reps / dt / 1e9
-    sample = (f"fp64 SPEC-faithful {'mc_flow' if cfg.iters else 'wmc_half_laplace'} "
-              f"(oracle/wmc_oracle.c, for_rows restatement) on a {crop_h}x{crop_w} crop of "
-              f"the {cfg.name} input, {reps} call(s) x {n} iteration(s), {dt:.1f} s")
-    return rate, threads, sample, "port"
+    if cfg.iters == 0:
+        wmap(work)
+    else:
+        flow(work, 1, cfg.dt)
+    one = time.perf_counter() - t0
+    n = max(1, min(cfg.iters or 50, int(budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    if cfg.iters == 0:
+        for _ in range(n):
+            wmap(work)
+    else:
+        flow(work, n, cfg.dt)
+    sec = time.perf_counter() - t0
+    rate = h * w * n / sec / 1e9
+    sample = (f"{what}; {'wmc_half_laplace' if cfg.iters == 0 else 'mc_flow'} on the full "
+              f"{h}x{w} first plane of the {cfg.name} input, {n} "
+              f"{'evaluation(s)' if cfg.iters == 0 else 'of its ' + str(cfg.iters) + ' iterations'}"
+              f" in {sec:.1f} s, {threads} threads")
+    return rate, threads, sample, kind, n, sec
 
 
 # ------------------------------------------------------------- b200 arm ----
@@ -254,6 +299,7 @@ def bench_b200(args, cfg):
         return torch.cuda.current_stream(dev).cuda_stream
 
     ws = None
+    prep = None  # per-step input restore of the in-place paths, run before each step's events
     if cfg.iters == 0:  # single map evaluation (cfg1)
         out = torch.empty(dev_in.shape, dtype=torch.float32, device=dev)
 
@@ -268,8 +314,10 @@ def bench_b200(args, cfg):
         band_bytes = dev_in.numel() * 4
         ipc_result = [0]
 
-        def step():
+        def prep():  # restore U^0 into the band (outside the timed region)
             assert L.cf_copy(band_ptr, dev_in.data_ptr(), band_bytes, sp) == 0
+
+        def step():
             ipc_result[0] = flow.run(cfg.iters, cfg.dt, stream=sp)
         launches_per_step = len(sharded.launch_schedule(cfg.iters, K))
     elif world > 1 and cfg.sharding == "rows":
@@ -284,10 +332,12 @@ def bench_b200(args, cfg):
             band_fn(*a)
         flow = sharded.ShardedFlow(lay, counted, dist, side_stream=torch.cuda.Stream(dev))
 
-        def step():
+        def prep():  # restore U^0 into the band (outside the timed region)
             buf_a[lay.band_slice()].copy_(dev_in)
-            res = flow.run(buf_a, buf_b, cfg.iters, cfg.dt)
-            return res
+
+        def step():
+            return flow.run(buf_a, buf_b, cfg.iters, cfg.dt)
+        prep()
         step()
         launches_per_step = n_band_calls[0]
     else:
@@ -309,8 +359,10 @@ def bench_b200(args, cfg):
                                            nb8, None, cur_sp())
                 assert rc == 0, rc
         else:
+            def prep():  # the filter is in place: restore U^0 (outside the timed region)
+                work.copy_(dev_in)
+
             def step():
-                work.copy_(dev_in)  # the filter is in place; restore U^0 each step
                 rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, cfg.iters, cfg.dt,
                                          ws.data_ptr(), nbytes, None, cur_sp())
                 assert rc == 0, rc
@@ -330,38 +382,51 @@ def bench_b200(args, cfg):
                  if l2_resident else None)
 
     def timed(fn, steps):
+        """Per-step CUDA events on the launching stream; the in-place paths'
+        input restore (prep) and the L2 flush run before each step's start
+        event.  Returns (median, mean) ms per step, each the max over ranks
+        (the median of the repetitions)."""
         barrier()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps)]
         for e0, e1 in evs:
+            if prep is not None:
+                prep()
             if flush_buf is not None:
                 flush_buf.zero_()
             e0.record(stream)
             fn()
             e1.record(stream)
         barrier()
-        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+        per = [e0.elapsed_time(e1) for e0, e1 in evs]
+        med, mean = statistics.median(per), sum(per) / steps
         if world > 1:
-            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
+            t = torch.tensor([med, mean], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms / steps
+            med, mean = (float(v) for v in t.tolist())
+        return med, mean
 
     # ---------------- device-resident timing (value) ----------------
     for _ in range(args.warmup):
+        if prep is not None:
+            prep()
         step()
     torch.cuda.synchronize(dev)
     run_step = step
     graph = world == 1  # one CUDA graph per step: no host launch gaps in the timed region
     if graph:
         g = torch.cuda.CUDAGraph()
+        if prep is not None:
+            prep()
         with torch.cuda.graph(g):
             step()
+        if prep is not None:
+            prep()
         g.replay()
         torch.cuda.synchronize(dev)
         run_step = g.replay
     with ClockSampler(local) as clk:
-        ms_step = timed(run_step, args.steps)
+        ms_step, ms_mean = timed(run_step, args.steps)
     if world > 1 and cfg.sharding == "rows" and args.halo != "ipc":
         assert int(flag.item()) == 0x7F7F7F7F, f"non-finite value in band launch {flag.item()}"
     if ws is not None:  # device non-finite flag of the last timed step
@@ -394,11 +459,13 @@ def bench_b200(args, cfg):
         # N > 1: gather the bands to rank 0 and compare with one GPU's filter
         # of the same input (whatever the halo transport, NCCL or IPC)
         if args.halo == "ipc":
+            prep()
             step()
             band = torch.empty((lay.r1 - lay.r0, cfg.w), dtype=torch.float32, device=dev)
             src_ptr = flow._row_ptr(flow.bufs[ipc_result[0]], lay.buf_row0, lay.r0)
             assert L.cf_copy(band.data_ptr(), src_ptr, band.numel() * 4, sp) == 0
         else:
+            prep()
             band = step()[lay.band_slice()].clone()
         torch.cuda.synchronize(dev)
         maxr = max(r1 - r0 for r0, r1 in sharded.band_bounds(cfg.h, world))
@@ -426,58 +493,13 @@ def bench_b200(args, cfg):
     value = updates_job / (ms_step * 1e-3) / 1e9
 
     # ---------------- dominant kernel: average launch duration ----------------
-    # The K-sweep kernel on the step's own geometry (all planes): a filter call
-    # of 2K iterations is exactly two K-sweep launches (+ a 4-byte memset).
-    kern_ms = None
-    if cfg.iters > 0 and not (world > 1):
-        import ctypes
-        reps = 10
-        kb = ctypes.c_int32(0)
-        assert int(L.cf_wmc_filter_launches(W, H, P, 2 * K)) == 2
-
-        def two_launches():
-            rc = L.cf_wmc_filter_f32(work.data_ptr(), W, H, W, P, H * W, 2 * K, cfg.dt,
-                                     ws.data_ptr(), nbytes, None, sp)
-            assert rc == 0, rc
-        if cfg.u8:  # measurement input: the widened frames (q/255)
-            work.copy_(dev_in.to(torch.float32).div_(255.0))
-        else:
-            work.copy_(dev_in)
-        for _ in range(2):
-            two_launches()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for _ in range(reps):
-            two_launches()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        kern_ms = e0.elapsed_time(e1) / (2 * reps)
-        kern_updates = n_px_local * K
-    elif cfg.iters > 0 and cfg.sharding == "rows":
-        # row bands: the K-sweep band kernel on this rank's own band
-        if args.halo == "ipc":
-            src_p, dst_p = flow.bufs[0], flow.bufs[1]
-        else:
-            src_p, dst_p = buf_a.data_ptr(), buf_b.data_ptr()
-        reps = 10
-
-        def band_launch(a, b):
-            rc = L.cf_wmc_sweeps_band_f32(a, lay.buf_row0, lay.rows, b, lay.buf_row0, cfg.w, cfg.h,
-                                          cfg.w, lay.r0, lay.r1, K, cfg.dt, 0, None, sp)
-            assert rc == 0, rc
-        band_launch(src_p, dst_p)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for i in range(reps):
-            band_launch(src_p if i % 2 == 0 else dst_p, dst_p if i % 2 == 0 else src_p)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        kern_ms = e0.elapsed_time(e1) / reps
-        kern_updates = (lay.r1 - lay.r0) * cfg.w * K
-    elif cfg.iters == 0:
-        kern_ms, kern_updates = ms_step, n_px_local
+    # Measured live over the timed region: the step is a chain of K-sweep
+    # launches of one kernel (u8: + one widening launch), so the kernel's
+    # average launch duration is the median step time over the step's sweep
+    # launches (inter-launch gaps included, so it can only understate).
+    sweep_launches = launches_per_step - (1 if cfg.u8 and world == 1 else 0)
+    kern_ms = ms_step / max(1, sweep_launches)
+    alg_bytes_step = algorithmic_bytes(cfg, n_px_local, u8_out=cfg.u8)
     peak, peak_src = peaks()
 
     # ---------------- end-to-end through the public API, host buffers ----------
@@ -636,16 +658,19 @@ def bench_b200(args, cfg):
         "scaling": "weak" if cfg.sharding == "images" else "strong",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded generator, DESIGN.md §6)",
-        "config": {
-            "workload": workload_name(cfg),
-            "iters": cfg.iters, "planes": cfg.planes, "h": cfg.h, "w": cfg.w,
+        "config": bench_config(cfg),
+        "impl_config": {
             "sweeps_per_launch": 1 if cfg.iters == 0 else K,
             "parallelism": (f"rowband{world}-{args.halo}" if cfg.sharding == "rows" and world > 1 else
                             f"images{world}" if world > 1 else "single"),
             "l2": ("inputs larger than L2 (126 MB)" if not l2_resident else
                    "working set fits in L2: 256 MiB flush between timed steps"),
-            "timing": ("one CUDA graph per step, CUDA events per step" if graph else
-                       "CUDA events per step (summed), max over ranks"),
+            "timing": ("one CUDA graph per step; CUDA events per step on the launching stream; "
+                       "median of the steps" if graph else
+                       "CUDA events per step on the launching stream; median of the steps, "
+                       "max over ranks") + ("; the in-place filter's input restore runs "
+                                            "before each step's start event" if prep else ""),
+            "ms_per_step_mean": round(ms_mean, 4),
         },
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4), "steps": e2e_steps,
@@ -658,19 +683,28 @@ def bench_b200(args, cfg):
         "selfcheck": selfcheck,
         "clocks": clk.summary(),
     }
-    if kern_ms is not None:
-        achieved = kern_updates * BYTES_PER_UPDATE / (kern_ms * 1e-3) / 1e9
-        res["roofline"] = {
-            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": f"wmc_sweeps_kernel<K={K}>" if cfg.iters else "wmc_sweeps_kernel<MAP>",
-            "kernel_ms": round(kern_ms, 4), "peak_source": peak_src,
-            "note": "algorithmic 8 B per pixel-update x updates per launch / launch time; "
-                    "traffic: physical DRAM bytes per launch from the committed ncu capture",
-        }
-        res["roofline"]["traffic"] = ncu_traffic(res["roofline"]["kernel"], H, W, P)
+    achieved = alg_bytes_step / (ms_step * 1e-3) / 1e9
+    kname = (f"wmc_sweeps_kernel<K={K}>" if cfg.iters else "wmc_sweeps_kernel<MAP>")
+    res["roofline"] = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4), "traffic": ncu_traffic(kname, H, W, P),
+        "kernel": kname + (" (+1 u8 widening launch)" if cfg.u8 and cfg.iters else ""),
+        "kernel_ms": round(kern_ms, 4), "launches_per_step": sweep_launches,
+        "algorithmic_bytes_per_step": alg_bytes_step,
+        "ncu_launch_ms": ncu_launch_ms(kname, H, W, P),
+        "peak_source": peak_src,
+        "note": "achieved = algorithmic bytes of the step (8 B per pixel-update, SURVEY.md "
+                "§8d) / the median step time of the timed region; kernel_ms = that step "
+                "time / the sweep launches of the step; traffic = physical DRAM bytes per "
+                "launch from the committed ncu --set full capture, ncu_launch_ms its "
+                "cold-cache duration",
+    }
+    assert kern_ms * sweep_launches <= ms_step * 1.0001
     if world == 1 and not args.no_cpu_baseline:
-        rate, cores, sample, kind = cpu_reference_sample(cfg, host[0] if host.ndim == 3 else host)
+        import numpy as np
+        plane0 = host[0] if host.ndim == 3 else host
+        img64 = plane0.astype(np.float64) / 255.0 if cfg.u8 else plane0.astype(np.float64)
+        rate, cores, sample, kind, _, _ = cpu_reference_sample(cfg, img64)
         res["cpu_baseline"] = {"value": round(rate, 4), "unit": UNIT, "cores": cores,
                                "kind": kind, "sample": sample}
     if world > 1:
@@ -680,6 +714,13 @@ def bench_b200(args, cfg):
 
 # -------------------------------------------------------- reference arm ----
 def bench_reference(args, cfg):
+    """The reference arm: the reference's CPU path (fp64 SPEC-faithful mc_flow
+    on the reference's own parallel::for_rows executor, oracle/_ref) on all
+    host threads, on the same workload -- the full-size first plane of the
+    config's seeded input, generated on the CPU by oracle/synth_ref.c (no
+    product library is loaded on this arm).  One step = n of the workload's
+    iterations on that image, n sized so the whole run stays within a few
+    minutes."""
     world, rank, _ = dist_env()
     if rank != 0:
         return None
@@ -687,47 +728,47 @@ def bench_reference(args, cfg):
 
     import oracle
     threads = os.cpu_count() or 1
-    crop = min(cfg.h, 2048), min(cfg.w, 2048)
-    full = make_input(cfg.__class__(**{**cfg.__dict__, "planes": 1}))
-    img = np.ascontiguousarray(full[:crop[0], :crop[1]], dtype=np.float64)
-    if cfg.u8:
-        img = img / 255.0
+    flow, wmap, kind, what = cpu_reference(threads)
+    plane0 = oracle.synth(cfg.w, cfg.h, cfg.seed(0), cfg.n_rects, cfg.n_discs, cfg.sigma,
+                          u8=cfg.u8, threads=threads)
+    img = plane0.astype(np.float64) / 255.0 if cfg.u8 else plane0.astype(np.float64)
+    del plane0
+
     def run(n):
         if cfg.iters == 0:
             for _ in range(n):
-                oracle.wmc_map_f64(img, threads)
+                wmap(img)
         else:
-            oracle.flow_f64(img, n, cfg.dt, threads)
-    # a step = n iterations (map evaluations) on the crop, n sized to ~2 s
-    # from the MARGINAL cost of an iteration ((run(4) - run(1)) / 3): each call
-    # allocates and first-touches its fp64 buffers (~0.15 s on a 2048^2 crop),
-    # which a 10-iteration step would report as half the reference's time
-    one, _ = marginal_cost(run)
-    n_it = max(1, min(cfg.iters or 50, int(2.0 / one)))
-
-    def sample():
-        run(n_it)
-    for _ in range(args.warmup):
-        sample()
+            flow(img, n, cfg.dt)
     t0 = time.perf_counter()
+    run(1)
+    one = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run ~2.5 min of CPU work
+    n_it = max(1, min(cfg.iters or 50, int(budget / max(one, 1e-6))))
+    for _ in range(args.warmup):
+        run(n_it)
+    per = []
     for _ in range(args.steps):
-        sample()
-    dt = time.perf_counter() - t0
-    rate = crop[0] * crop[1] * n_it * args.steps / dt / 1e9
-    desc = (f"fp64 SPEC-faithful {'wmc_half_laplace' if cfg.iters == 0 else 'mc_flow'} "
-            f"(oracle/wmc_oracle.c, the reference algorithm restated; for_rows executor) on a "
-            f"{crop[0]}x{crop[1]} crop of the {cfg.name} input, {n_it} iteration(s) per step")
+        t0 = time.perf_counter()
+        run(n_it)
+        per.append(time.perf_counter() - t0)
+    sec = statistics.median(per)
+    rate = cfg.h * cfg.w * n_it / sec / 1e9
+    desc = (f"{what}; {'wmc_half_laplace' if cfg.iters == 0 else 'mc_flow'} on the full "
+            f"{cfg.h}x{cfg.w} first plane of the {cfg.name} input (oracle/synth_ref.c), "
+            f"{n_it} {'evaluation(s)' if cfg.iters == 0 else 'of its ' + str(cfg.iters) + ' iterations'}"
+            f" per step, median of {args.steps} steps, {threads} threads")
     return {
         "impl": "reference", "metric": METRIC, "value": round(rate, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
         "scaling": "weak" if cfg.sharding == "images" else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generator, DESIGN.md §6)",
-        "config": {"workload": workload_name(cfg), "iters": cfg.iters, "planes": cfg.planes,
-                   "h": cfg.h, "w": cfg.w, "parallelism": f"cpu{threads}",
-                   "sample": f"{crop[0]}x{crop[1]} crop, {n_it} iteration(s) per step"},
+        "config": bench_config(cfg),
+        "impl_config": {"parallelism": f"cpu{threads}",
+                        "sample": f"{n_it} iteration(s) of the full first plane per step"},
         "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": threads,
-                         "kind": "port", "sample": desc},
+                         "kind": kind, "sample": desc},
         "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -750,7 +791,7 @@ def main():
                          "CUDA IPC peer memory")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    from paper_1903_07189_b200.configs import CONFIGS, SUPPLEMENTAL
+    CONFIGS, SUPPLEMENTAL = load_configs()
     if args.all:
         with open(args.all, "w") as f:
             for name, c in list(CONFIGS.items()) + list(SUPPLEMENTAL.items()):

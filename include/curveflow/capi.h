@@ -299,6 +299,41 @@ CF_API int cf_synth_u8(uint8_t* out, int32_t w, int32_t h, int64_t pitch, uint64
 /* ---------------------------------------------------------------------- */
 CF_API void cf_kernel_bank_x12(int32_t* out72);
 
+/* ---------------------------------------------------------------------- */
+/* The SPEC-faithful fp64 path (csrc/wmc_f64.cu)            */
+/* fp64 images (the reference computes in fp64) and the */
+/* reference CPU path's own arithmetic: per kernel s = s + w*x over the     */
+/* row-major taps with w = n/12 rounded to fp64, multiply and add rounded   */
+/* separately, strict-< first-minimum scan; */
+/* flow step u + dt*d.  Results are BIT-IDENTICAL to the  */
+/* reference CPU implementation for finite images (not a tolerance); the    */
+/* price is the FP64 pipe (about 60 DP operations per pixel-update).        */
+/* Layout and conventions as the fp32 entry points, elements of 8 bytes.    */
+/* ---------------------------------------------------------------------- */
+/* wmc_half_laplace in fp64 (replaces SPEC.md:171's operation bit-exactly). */
+CF_API int cf_wmc_map_f64(const double* in, double* out, int32_t w, int32_t h, int64_t pitch,
+                          int32_t planes, int64_t plane_stride, void* stream);
+/* Workspace of cf_wmc_filter_f64 / cf_wmc_filter_u8_f64: 256-byte header
+ * (non-finite flag) + one fp64 image of the given geometry. */
+CF_API size_t cf_wmc_filter_f64_workspace_bytes(int32_t w, int32_t h, int64_t pitch,
+                                                int32_t planes, int64_t plane_stride);
+/* mc_flow in fp64, in place, Jacobi (replaces SPEC.md:256's operation
+ * bit-exactly).  dt in (0, 1], iters >= 0 (0: identity).  first_bad_iter
+ * non-null: synchronises `stream`, returns CF_ENONFINITE naming the first
+ * iteration that produced a non-finite value. */
+CF_API int cf_wmc_filter_f64(double* img, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                             int64_t plane_stride, int32_t iters, double dt, void* workspace,
+                             size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
+/* u8 planes widened as (double)q / 255.0 (IEEE division), then
+ * cf_wmc_filter_f64 into `out` (fp64 planes of the given geometry). */
+CF_API int cf_wmc_filter_u8_f64(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
+                                double* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                                int64_t plane_stride, int32_t iters, double dt, void* workspace,
+                                size_t workspace_bytes, int32_t* first_bad_iter, void* stream);
+/* Read back the fp64 filter's non-finite flag (synchronises `stream`). */
+CF_API int cf_wmc_filter_f64_query_nonfinite(const void* workspace, int32_t* first_bad_iter,
+                                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -153,8 +153,15 @@ def flow_f32(img, iters, dt=1.0, threads=None):
     return (a3[0] if a.ndim == 2 else a3), bad.value
 
 
-def flow_f64(img, iters, dt=1.0, threads=None):
-    a = np.array(img, dtype=np.float64, order="C", copy=True)
+def _f64_work(img, inplace):
+    if inplace:  # filter a C-contiguous float64 array in place (no copy of big inputs)
+        assert img.dtype == np.float64 and img.flags.c_contiguous
+        return img
+    return np.array(img, dtype=np.float64, order="C", copy=True)
+
+
+def flow_f64(img, iters, dt=1.0, threads=None, inplace=False):
+    a = _f64_work(img, inplace)
     h, w = a.shape
     bad = C.c_int32(0)
     rc = lib().or_flow_f64(a.ctypes.data, w, h, int(iters), float(dt), _threads(threads),
@@ -163,11 +170,11 @@ def flow_f64(img, iters, dt=1.0, threads=None):
     return a, bad.value
 
 
-def ref_flow_f64(img, iters, dt=1.0, threads=None):
+def ref_flow_f64(img, iters, dt=1.0, threads=None, inplace=False):
     L = ref_lib()
     if L is None:
         raise RuntimeError("oracle/_ref/libcf_ref.so not built")
-    a = np.array(img, dtype=np.float64, order="C", copy=True)
+    a = _f64_work(img, inplace)
     h, w = a.shape
     bad = C.c_int32(0)
     rc = L.ref_flow_f64(a.ctypes.data, w, h, int(iters), float(dt), _threads(threads),

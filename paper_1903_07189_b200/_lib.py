@@ -84,6 +84,14 @@ SIGNATURES = {
     "cf_synth_f32": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_synth_u8": (C.c_int, [_vp, _i32, _i32, _i64, _u64, _i32, _i32, _f64, _i32]),
     "cf_kernel_bank_x12": (None, [_pi32]),
+    # the SPEC-faithful fp64 path (csrc/wmc_f64.cu)
+    "cf_wmc_map_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _vp]),
+    "cf_wmc_filter_f64_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32, _i64]),
+    "cf_wmc_filter_f64": (C.c_int, [_vp, _i32, _i32, _i64, _i32, _i64, _i32, _f64, _vp, _sz,
+                                    _pi32, _vp]),
+    "cf_wmc_filter_u8_f64": (C.c_int, [_vp, _i64, _i64, _vp, _i32, _i32, _i64, _i32, _i64,
+                                       _i32, _f64, _vp, _sz, _pi32, _vp]),
+    "cf_wmc_filter_f64_query_nonfinite": (C.c_int, [_vp, _pi32, _vp]),
 }
 
 

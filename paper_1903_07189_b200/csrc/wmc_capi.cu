@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <tuple>
 #include <mutex>
 #include <vector>
@@ -310,16 +311,20 @@ struct FlowKey {
     int32_t iters; uint32_t dt; void* ws;
     const float* f; uint32_t lambda; float* d; float* d_ws; uint32_t alpha;
     uint8_t* o8; int64_t o8_pitch, o8_plane;
-    auto tie() const {
-        return std::tie(dev, src0, src_u8, src_pitch, src_plane, out, w, h, pitch, planes,
-                        plane_stride, iters, dt, ws, f, lambda, d, d_ws, alpha, o8, o8_pitch,
-                        o8_plane);
+    // field-by-field bytes (no padding): the cache's key
+    std::string bytes() const {
+        std::string k;
+        auto put = [&k](const auto& v) { k.append(reinterpret_cast<const char*>(&v), sizeof(v)); };
+        put('F'); put(src0); put(src_u8); put(src_pitch); put(src_plane); put(out); put(w);
+        put(h); put(pitch); put(planes); put(plane_stride); put(iters); put(dt); put(ws); put(f);
+        put(lambda); put(d); put(d_ws); put(alpha); put(o8); put(o8_pitch); put(o8_plane);
+        return k;
     }
-    bool operator==(const FlowKey& o) const { return tie() == o.tie(); }
 };
 
 struct GraphEntry {
-    FlowKey key;
+    int dev = 0;
+    std::string key;                 // argument bytes of the run (per entry point family)
     cudaGraphExec_t exec = nullptr;  // null: seen once, not captured yet
     bool no_graph = false;           // capture failed once: plain launches for this key
     uint64_t last_use = 0;
@@ -350,7 +355,7 @@ uint32_t f32_bits(float v) {
 // and cudaGraphLaunch (an exec must not be evicted mid-launch); a key's
 // first, plain run happens outside it.
 template <typename Fn>
-int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
+int run_cached(int dev, const std::string& key, cudaStream_t s, Fn&& enqueue) {
     if (!graphs_enabled()) return enqueue(s);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
@@ -362,7 +367,7 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
     const uint64_t now = ++g_graph_clock;
     GraphEntry* hit = nullptr;
     for (GraphEntry& e : g_graphs)
-        if (e.key == key) { hit = &e; break; }
+        if (e.dev == dev && e.key == key) { hit = &e; break; }
     if (!hit) {  // first sighting: remember the key, launch directly
         if (g_graphs.size() >= kGraphCap) {
             auto lru = std::min_element(g_graphs.begin(), g_graphs.end(),
@@ -373,6 +378,7 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
             g_graphs.erase(lru);
         }
         GraphEntry e;
+        e.dev = dev;
         e.key = key;
         e.last_use = now;
         g_graphs.push_back(e);
@@ -385,8 +391,8 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
         return enqueue(s);
     }
     if (!hit->exec) {  // second sighting: capture on the device's capture stream
-        if ((int)g_capture_streams.size() <= key.dev) g_capture_streams.resize(key.dev + 1, nullptr);
-        cudaStream_t& cap = g_capture_streams[key.dev];
+        if ((int)g_capture_streams.size() <= dev) g_capture_streams.resize(dev + 1, nullptr);
+        cudaStream_t& cap = g_capture_streams[dev];
         bool ok = cap || cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess;
         if (ok && cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
             const int rc = enqueue(cap);
@@ -422,6 +428,16 @@ int run_cached(const FlowKey& key, cudaStream_t s, Fn&& enqueue) {
 
 // Shared with wmc_io.cu / wmc_shard.cpp; hidden (not part of the C-ABI).
 extern "C" void cf_internal_set_cuda_error(int e) { g_last_cuda = e; }
+// The same cache for the other entry-point families (wmc_f64.cu): `key` is
+// the caller's argument bytes (padding-free), `enqueue(ctx, stream)` the run.
+extern "C" int cf_internal_graph_run(const void* key, size_t key_len, void* stream,
+                                     int (*enqueue)(void* ctx, void* stream), void* ctx) {
+    int dev = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    return run_cached(dev, std::string(static_cast<const char*>(key), key_len),
+                      (cudaStream_t)stream,
+                      [&](cudaStream_t st) { return enqueue(ctx, (void*)st); });
+}
 extern "C" int cf_internal_schedule(int32_t iters, int32_t levels, int32_t* out, int32_t cap) {
     const std::vector<int> ks = schedule(iters, levels);
     if ((int32_t)ks.size() > cap) return -1;
@@ -594,7 +610,7 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
     key.ws = workspace; key.f = dterm.f; key.lambda = f32_bits(dterm.lambda);
     key.d = dterm.d; key.d_ws = dterm.d_ws; key.alpha = f32_bits(dterm.alpha);
     key.o8 = out8.p; key.o8_pitch = out8.pitch; key.o8_plane = out8.plane;
-    const int rc = run_cached(key, s, [&](cudaStream_t st) {
+    const int rc = run_cached(key.dev, key.bytes(), s, [&](cudaStream_t st) {
         return enqueue_flow(src0, src_u8, src_pitch, src_plane, out, w, h, pitch, planes,
                             plane_stride, iters, dt, workspace, st, dterm, out8);
     });

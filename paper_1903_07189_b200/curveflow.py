@@ -87,35 +87,54 @@ def _as_planes(t):
     raise ValueError("image must be (H, W) or (P, H, W)")
 
 
-def _device_image(img):
+def _precision(img, precision):
+    """"fp32" (the canonical fp32 sequence) or "fp64" (the
+    reference CPU path's own fp64 arithmetic, bit-identical to it, DESIGN.md
+    §3.6).  None: fp64 for float64 torch tensors, fp32 otherwise."""
+    if precision is None:
+        torch = _torch()
+        return "fp64" if isinstance(img, torch.Tensor) and img.dtype == torch.float64 else "fp32"
+    if precision not in ("fp32", "fp64"):
+        raise ValueError("precision must be 'fp32' or 'fp64'")
+    return precision
+
+
+def _device_image(img, precision="fp32"):
     torch = _torch()
+    dt_np, dt_t = (np.float64, torch.float64) if precision == "fp64" else (np.float32,
+                                                                            torch.float32)
     if isinstance(img, np.ndarray):
-        return torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda(), True
+        return torch.from_numpy(np.ascontiguousarray(img, dtype=dt_np)).cuda(), True
     if not isinstance(img, torch.Tensor):
         raise TypeError("image must be a torch.Tensor or numpy.ndarray")
     if not img.is_cuda:
-        return img.to(dtype=torch.float32).contiguous().cuda(), True
-    if img.dtype != torch.float32:
-        raise TypeError("device images must be float32")
+        return img.to(dtype=dt_t).contiguous().cuda(), True
+    if img.dtype != dt_t:
+        raise TypeError(f"device images must be {'float64' if precision == 'fp64' else 'float32'}"
+                        f" for precision={precision!r}")
     return img, False
 
 
-def wmc_half_laplace(img):
-    """Discrete WMC map d_m; returns a new image."""
+def wmc_half_laplace(img, *, precision=None):
+    """Discrete WMC map d_m; returns a new image.
+    precision="fp64" (or a float64 device tensor): the reference's fp64
+    arithmetic, bit-identical to the reference CPU path (cf_wmc_map_f64)."""
     torch = _torch()
-    src, host = _device_image(img)
+    prec = _precision(img, precision)
+    src, host = _device_image(img, prec)
     x, squeeze = _as_planes(src)
     x = x if x.stride(-1) == 1 else x.contiguous()
     P, H, W = x.shape
-    out = torch.empty((P, H, W), dtype=torch.float32, device=x.device)
+    out = torch.empty((P, H, W), dtype=src.dtype, device=x.device)
     if P and H and W:
         pitch, plane = x.stride(1), x.stride(0)
         if out.stride(1) != pitch or out.stride(0) != plane:
             x = x.contiguous()
             pitch, plane = x.stride(1), x.stride(0)
+        fn = lib().cf_wmc_map_f64 if prec == "fp64" else lib().cf_wmc_map_f32
         with torch.cuda.device(x.device):
-            check(lib().cf_wmc_map_f32(x.data_ptr(), out.data_ptr(), W, H, pitch, P, plane,
-                                       _stream_ptr(torch, x.device)), "wmc_half_laplace")
+            check(fn(x.data_ptr(), out.data_ptr(), W, H, pitch, P, plane,
+                     _stream_ptr(torch, x.device)), "wmc_half_laplace")
     res = out[0] if squeeze else out
     if host:
         return res.cpu().numpy() if isinstance(img, np.ndarray) else res.cpu()
@@ -127,32 +146,38 @@ def workspace_bytes(h: int, w: int, planes: int = 1) -> int:
 
 
 def mc_flow(img, cfg: FlowConfig, *, check_finite: bool = True, workspace=None,
-            inplace: bool = False):
+            inplace: bool = False, precision=None):
     """Mean-curvature flow, scheme=half_laplace.
 
     Returns U^iters.  Raises FlowError(iteration) if an iterate becomes
     non-finite.  ``inplace=True`` (device tensors only)
     overwrites ``img``.  ``check_finite=False`` skips the host sync the
     diagnostic needs (the device-side check still runs).
+    ``precision="fp64"`` (or a float64 device tensor): fp64 images and the
+    reference's fp64 arithmetic, bit-identical to the reference CPU path
+    (cf_wmc_filter_f64).
     """
     torch = _torch()
     cfg.validate()
-    src, host = _device_image(img)
+    prec = _precision(img, precision)
+    src, host = _device_image(img, prec)
     if inplace and (host or not src.is_contiguous()):
         raise ValueError("inplace=True needs a contiguous CUDA tensor")
     x = src if inplace else src.clone(memory_format=torch.contiguous_format)
     x3, squeeze = _as_planes(x)
     P, H, W = x3.shape
     if cfg.iters > 0 and P and H and W:
-        nbytes = int(lib().cf_wmc_filter_workspace_bytes(W, H, W, P, H * W))
+        f64 = prec == "fp64"
+        nbytes = int((lib().cf_wmc_filter_f64_workspace_bytes if f64 else
+                      lib().cf_wmc_filter_workspace_bytes)(W, H, W, P, H * W))
         if workspace is None or workspace.numel() < nbytes:
             workspace = torch.empty(nbytes, dtype=torch.uint8, device=x3.device)
         bad = C.c_int32(0)
+        fn = lib().cf_wmc_filter_f64 if f64 else lib().cf_wmc_filter_f32
         with torch.cuda.device(x3.device):
-            rc = lib().cf_wmc_filter_f32(x3.data_ptr(), W, H, W, P, H * W, int(cfg.iters),
-                                         float(cfg.dt), workspace.data_ptr(), nbytes,
-                                         C.byref(bad) if check_finite else None,
-                                         _stream_ptr(torch, x3.device))
+            rc = fn(x3.data_ptr(), W, H, W, P, H * W, int(cfg.iters), float(cfg.dt),
+                    workspace.data_ptr(), nbytes, C.byref(bad) if check_finite else None,
+                    _stream_ptr(torch, x3.device))
         if rc == CF_ENONFINITE:
             raise FlowError(bad.value)
         check(rc, "mc_flow")
@@ -170,8 +195,8 @@ def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=
     (rint(clamp(U, 0, 1) * 255), the reference's save-time rounding)."""
     torch = _torch()
     cfg.validate()
-    if out_dtype not in ("f32", "u8"):
-        raise ValueError("out_dtype must be 'f32' or 'u8'")
+    if out_dtype not in ("f32", "u8", "f64"):
+        raise ValueError("out_dtype must be 'f32', 'u8' or 'f64'")
     if isinstance(img_u8, np.ndarray):
         src = torch.from_numpy(np.ascontiguousarray(img_u8, dtype=np.uint8)).cuda()
         host = True
@@ -189,6 +214,11 @@ def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=
             out = torch.empty((P, H, W), dtype=torch.uint8, device=s3.device)
         nbytes = int(lib().cf_wmc_filter_u8_u8_workspace_bytes(W, H, P))
         need_ws = True
+    elif out_dtype == "f64":  # fp64 widening q/255 + the reference's fp64 arithmetic
+        if out is None:
+            out = torch.empty((P, H, W), dtype=torch.float64, device=s3.device)
+        nbytes = int(lib().cf_wmc_filter_f64_workspace_bytes(W, H, W, P, H * W))
+        need_ws = True
     else:
         if out is None:
             out = torch.empty((P, H, W), dtype=torch.float32, device=s3.device)
@@ -200,7 +230,11 @@ def mc_flow_u8(img_u8, cfg: FlowConfig, *, check_finite: bool = True, workspace=
     bad_ptr = C.byref(bad) if check_finite else None
     with torch.cuda.device(s3.device):
         strm = _stream_ptr(torch, s3.device)
-        if out_dtype == "u8":
+        if out_dtype == "f64":
+            rc = lib().cf_wmc_filter_u8_f64(s3.data_ptr(), W, H * W, out.data_ptr(), W, H, W, P,
+                                            H * W, int(cfg.iters), float(cfg.dt), ptr(workspace),
+                                            nbytes, bad_ptr, strm)
+        elif out_dtype == "u8":
             rc = lib().cf_wmc_filter_u8_u8(s3.data_ptr(), W, H * W, out.data_ptr(), W, H * W, W, H,
                                            P, int(cfg.iters), float(cfg.dt), ptr(workspace),
                                            nbytes, bad_ptr, strm)
