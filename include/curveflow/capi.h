@@ -188,6 +188,9 @@ CF_API int cf_wmc_sweeps_band_peer_f32(const float* src, int32_t src_row0, int32
 /* CUDA IPC / event plumbing for that protocol (handles are 64 bytes).       */
 CF_API int cf_device_alloc(size_t bytes, void** dptr);
 CF_API int cf_device_free(void* dptr);
+/* cudaMemsetAsync of `bytes` bytes to `value` on `stream` (the band flow's
+ * non-finite flag is reset with 0x7f before every run). */
+CF_API int cf_device_memset(void* dptr, int value, size_t bytes, void* stream);
 CF_API int cf_copy(void* dst, const void* src, size_t bytes, void* stream);
 CF_API int cf_ipc_mem_handle(const void* dptr, void* handle_out);
 CF_API int cf_ipc_open_mem(const void* handle, void** dptr);

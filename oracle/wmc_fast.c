@@ -9,7 +9,7 @@
  * 26-28), in the same operand order, with the same roundings:
  *   - fp32 canonical:  wmc_px_f32_full() + the flow step
  *     fmaf(dt, H^w, u) of or_flow_f32, or the map's near-tie rule
- *     (near_tie_f32 / wmc_map_px_f32);
+ *     (map_best_f32 / wmc_map_px_f32);
  *   - fp64 SPEC-faithful: wmc_px_f64() (row-major taps, s = s + w*x, weights
  *     n/12 rounded once, strict-< first-minimum) + u + dt*H (or_flow_f64).
  * Only the loop structure differs: a row's interior columns run as one loop
@@ -106,12 +106,12 @@ static void row32(const float* R0, const float* R1, const float* R2, float* O, i
         const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
         px32 o;
         wmc_px_f32_full(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x], R2[xp], &o);
-        const float hw = o.best * C12;
         if (mode == 0) {
-            O[x] = fmaf(dt, hw, R1[x]);
+            O[x] = fmaf(dt, o.best * C12, R1[x]);
         } else {
-            O[x] = hw;
-            tie[x] = (int8_t)near_tie_f32(&o);
+            int t;
+            O[x] = map_best_f32(&o, &t) * C12;
+            tie[x] = (int8_t)t;
         }
     }
     if (mode == 0) {
@@ -128,13 +128,26 @@ static void row32(const float* R0, const float* R1, const float* R2, float* O, i
             float DS[8], best, n12u;
             CANON_BEST(R0[x - 1], R0[x], R0[x + 1], R1[x - 1], R1[x], R1[x + 1], R2[x - 1], R2[x],
                        R2[x + 1], best, n12u);
-            float T = 3.0e38f, t;
-#define TMIN(k) t = fabsf(DS[k] + best); T = t < T ? t : T;
-            TMIN(0) TMIN(1) TMIN(2) TMIN(3) TMIN(4) TMIN(5) TMIN(6) TMIN(7)
-#undef TMIN
-            const float tau = fmaf(fabsf(n12u), 0x1.8p-19f, fabsf(best) * 0x1.0p-20f);
-            tie[x] = (int8_t)((T <= tau) & (T < fabsf(best)));
-            O[x] = best * C12;
+            /* map_best_f32 (wmc_px.h), written for the vectoriser */
+            uint32_t U, v;
+            memcpy(&U, &DS[0], 4);
+            int32_t S = (int32_t)U;
+            for (int k = 1; k < 8; ++k) {
+                memcpy(&v, &DS[k], 4);
+                U = v < U ? v : U;
+                S = (int32_t)v < S ? (int32_t)v : S;
+            }
+            float P, N;
+            memcpy(&P, &U, 4);
+            memcpy(&N, &S, 4);
+            const float xs = P + N;
+            float b = xs > 0.0f ? N : P;
+            const int slow = (U != (uint32_t)S) & !((xs > 0.0f) | (xs < 0.0f));
+            b = slow ? best : b;
+            const float tau = fmaf(fabsf(n12u), 0x1.8p-19f, fabsf(b) * 0x1.0p-20f);
+            const float ax = fabsf(xs);
+            tie[x] = (int8_t)((ax <= tau) & (ax < fabsf(b)));
+            O[x] = b * C12;
         }
     }
 }

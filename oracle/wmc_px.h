@@ -7,6 +7,7 @@
 #define CF_ORACLE_WMC_PX_H
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 #include <pthread.h>
 
 static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -129,17 +130,40 @@ static inline float wmc_px_f32(float a, float b, float c, float l, float u, floa
     return o.best * C12;
 }
 
-/* Opposite-sign near-tie test of the map:
- * T = min_k |fl(D_k + D_m)|, tau = fmaf(|n12u|, 1.5*2^-18, fl(|D_m| * 2^-20)),
- * tie iff T <= tau && T < |D_m|. */
-static inline int near_tie_f32(const px32* o) {
-    float T = 3.0e38f;
-    for (int k = 0; k < 8; ++k) {
-        float t = fabsf(o->D[k] + o->best);
-        T = t < T ? t : T;
+/* The map's selection and opposite-sign near-tie test.
+ * U = min of the eight D_k's bit patterns as unsigned, S = as signed: when
+ * both signs occur (U != S), P = U is the smallest-magnitude non-negative
+ * D and N = S the smallest-magnitude negative one, so x = fl(P + N) says
+ * which is the minimum magnitude (x > 0: N, x < 0: P) and |x| is the
+ * distance of the opposite-sign runner-up, i.e. min_k |fl(D_k + D_m)| over
+ * the opposite-sign k (same-sign k are >= 2|D_m| and never near a tie).
+ * When all D share a sign, U == S is the minimum.  Only an exact
+ * opposite-sign tie (or a NaN x) needs the first index: the tournament.
+ * For finite, non-overflowing D this is exactly the strict-< first-minimum
+ * scan of SPEC.md:195 and the T = min_k |fl(D_k + D_m)| rule of round 1.
+ * tau = fmaf(|n12u|, 1.5*2^-19, fl(|D_m| * 2^-20)); tie iff |x| <= tau and
+ * |x| < |D_m|. */
+static inline float map_best_f32(const px32* o, int* tie) {
+    uint32_t U, v;
+    int32_t S, sv;
+    memcpy(&U, &o->D[0], 4);
+    S = (int32_t)U;
+    for (int k = 1; k < 8; ++k) {
+        memcpy(&v, &o->D[k], 4);
+        sv = (int32_t)v;
+        U = v < U ? v : U;
+        S = sv < S ? sv : S;
     }
-    const float tau = fmaf(fabsf(o->n12u), 0x1.8p-19f, fabsf(o->best) * 0x1.0p-20f);
-    return T <= tau && T < fabsf(o->best);
+    float P, N;
+    memcpy(&P, &U, 4);
+    memcpy(&N, &S, 4);
+    const float x = P + N;
+    float b = x > 0.0f ? N : P;
+    if (U != (uint32_t)S && !(x > 0.0f || x < 0.0f)) b = o->best; /* exact tie / NaN */
+    const float tau = fmaf(fabsf(o->n12u), 0x1.8p-19f, fabsf(b) * 0x1.0p-20f);
+    const float ax = fabsf(x);
+    *tie = (ax <= tau) && (ax < fabsf(b));
+    return b;
 }
 
 /* The map: canonical fp32, with opposite-sign near-ties resolved by the
@@ -148,19 +172,21 @@ static inline float wmc_map_px_f32(float a, float b, float c, float l, float u, 
                                    float f, float g, int* tie) {
     px32 o;
     wmc_px_f32_full(a, b, c, l, u, r, e, f, g, &o);
-    if (near_tie_f32(&o)) {
+    int t;
+    const float best = map_best_f32(&o, &t);
+    if (t) {
         pthread_once(&hw_once, init_hw64);
         const double nb[9] = {a, b, c, l, u, r, e, f, g};
-        double best = 0.0;
+        double best64 = 0.0;
         for (int i = 0; i < 8; ++i) {
             double s = 0.0;
-            for (int t = 0; t < 9; ++t) s = s + HW64[i][t / 3][t % 3] * nb[t];
-            if (i == 0 || fabs(s) < fabs(best)) best = s;
+            for (int k = 0; k < 9; ++k) s = s + HW64[i][k / 3][k % 3] * nb[k];
+            if (i == 0 || fabs(s) < fabs(best64)) best64 = s;
         }
         if (tie) *tie = 1;
-        return (float)best;
+        return (float)best64;
     }
     if (tie) *tie = 0;
-    return o.best * C12;
+    return best * C12;
 }
 #endif

@@ -51,6 +51,7 @@ SIGNATURES = {
                                               _i32, _i32, _vp]),
     "cf_device_alloc": (C.c_int, [_sz, C.POINTER(_vp)]),
     "cf_device_free": (C.c_int, [_vp]),
+    "cf_device_memset": (C.c_int, [_vp, C.c_int, _sz, _vp]),
     "cf_copy": (C.c_int, [_vp, _vp, _sz, _vp]),
     "cf_ipc_mem_handle": (C.c_int, [_vp, _vp]),
     "cf_ipc_open_mem": (C.c_int, [_vp, C.POINTER(_vp)]),

@@ -20,7 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/curveflow/capi.h"
-#include "wmc_sweep.cuh"
+#include "wmc_map.cuh"
 
 namespace {
 
@@ -191,6 +191,56 @@ int launch(const cfk::SweepParams& p, int K, const DevInfo& d, cudaStream_t s) {
     }
 }
 
+
+// The streaming map (csrc/wmc_map.cuh): one warp per 256 columns x strip;
+// strips sized so waves x (rows + warm-up) is minimal over the resident slots.
+int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+               int64_t plane_stride, const DevInfo& d, cudaStream_t s) {
+    constexpr size_t smem = (size_t)cfk::kMapWarps * cfk::kMapRing * cfk::kMapRowBytes;
+    static std::atomic<int> occ{-1};  // resident warps per SM (same on every B200)
+    int warps = occ.load(std::memory_order_acquire);
+    if (warps < 0) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(cfk::wmc_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cfk::wmc_map_kernel,
+                                                          32 * cfk::kMapWarps, smem) != cudaSuccess ||
+            blocks <= 0)
+            blocks = 2;
+        warps = blocks * cfk::kMapWarps;
+        occ.store(warps, std::memory_order_release);
+    }
+    cfk::MapParams p{};
+    p.src = in; p.dst = out;
+    p.src_pitch = p.dst_pitch = pitch;
+    p.src_plane = p.dst_plane = plane_stride;
+    p.w = w; p.h = h; p.planes = planes;
+    p.n_pairs = (w + 2 * cfk::kMapChunk - 1) / (2 * cfk::kMapChunk);
+    p.st128 = ((reinterpret_cast<uintptr_t>(out) & 15) == 0 && (pitch & 3) == 0 &&
+               (planes == 1 || (plane_stride & 3) == 0)) ? 1 : 0;
+    const int64_t slots = (int64_t)d.sms * warps;
+    const int64_t cols = (int64_t)p.n_pairs * planes;
+    double best_cost = 1e300;
+    int best = 1;
+    const int max_strips = std::max(1, h / 8);
+    for (int ns = 1; ns <= max_strips; ++ns) {
+        const int sr = (h + ns - 1) / ns;
+        const int64_t tasks = cols * ((h + sr - 1) / sr);
+        const int64_t waves = (tasks + slots - 1) / slots;
+        const double cost = (double)waves * (sr + 8.0);  // + warm-up / fixed cost (rows)
+        if (cost < best_cost * 0.999) { best_cost = cost; best = ns; }
+        if (tasks > slots * 32) break;
+    }
+    p.strip_rows = (h + best - 1) / best;
+    p.n_strips = (h + p.strip_rows - 1) / p.strip_rows;
+    const int64_t tasks = cols * p.n_strips;
+    const int64_t blocks = (tasks + cfk::kMapWarps - 1) / cfk::kMapWarps;
+    if (blocks > INT_MAX) return CF_EINVAL;
+    cfk::wmc_map_kernel<<<(unsigned)blocks, 32 * cfk::kMapWarps, smem, s>>>(p);
+    CF_CUDA(cudaGetLastError());
+    return CF_OK;
+}
 
 bool shape_ok(int32_t w, int32_t h, int64_t pitch, int32_t planes, int64_t plane_stride) {
     if (w <= 0 || h <= 0 || planes <= 0 || pitch < w) return false;
@@ -494,22 +544,16 @@ CF_API int cf_wmc_map_f32(const float* in, float* out, int32_t w, int32_t h, int
     if (!in || !out || in == out || !shape_ok(w, h, pitch, planes, plane_stride)) return CF_EINVAL;
     DevInfo d;
     if (int rc = device_info(&d)) return rc;
-    cfk::SweepParams p{};
-    p.src = in; p.dst = out;
-    p.src_pitch = p.dst_pitch = pitch;
-    p.src_plane = p.dst_plane = plane_stride;
-    p.src_row0 = p.dst_row0 = 0;
-    p.w = w; p.h = h; p.y0 = 0; p.y1 = h; p.planes = planes;
-    p.dt = 0.f; p.iter_base = 0; p.flag = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
     if ((int64_t)w * h * planes <= kFlatMapPixels) {  // latency-bound size: flat kernel
         const int64_t pairs = (int64_t)((w + 1) / 2) * h * planes;
         const int64_t blocks = std::min<int64_t>((pairs + 255) / 256, (int64_t)d.sms * 16);
-        cfk::wmc_map_flat_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        cfk::wmc_map_flat_kernel<<<(unsigned)blocks, 256, 0, s>>>(
             in, out, w, h, pitch, plane_stride, pitch, plane_stride, planes);
         CF_CUDA(cudaGetLastError());
         return CF_OK;
     }
-    return launch<cfk::kModeMap>(p, 1, d, (cudaStream_t)stream);
+    return launch_map(in, out, w, h, pitch, planes, plane_stride, d, s);
 }
 
 CF_API size_t cf_wmc_filter_workspace_bytes(int32_t w, int32_t h, int64_t pitch, int32_t planes,

@@ -126,13 +126,18 @@ __global__ void __launch_bounds__(32 * kWarps) wmc_f64_kernel(const Step64 p) {
     auto row = [&](int y) { return src + (int64_t)min(max(y, 0), p.h - 1) * p.src_pitch; };
     const double* rm = row(y0 - 1);
     const double* r0 = row(y0);
+    const double* r1 = row(y0 + 1);
     double a = __ldg(rm + xl), b = __ldg(rm + xc), c = __ldg(rm + xr);
     double l = __ldg(r0 + xl), u = __ldg(r0 + xc), r = __ldg(r0 + xr);
+    double e = __ldg(r1 + xl), f = __ldg(r1 + xc), g = __ldg(r1 + xr);
+    // software pipeline: row y+2's loads are in flight while row y computes
+    // (the DMULs otherwise wait on their own row's loads: long-scoreboard)
+    const double* rn = row(y0 + 2);
     bool bad = false;
 #pragma unroll 3  // the window's register rotation disappears (renaming)
     for (int y = y0; y < y1; ++y) {
-        const double* rp = row(y + 1);
-        const double e = __ldg(rp + xl), f = __ldg(rp + xc), g = __ldg(rp + xr);
+        const double ne = __ldg(rn + xl), nf = __ldg(rn + xc), ng = __ldg(rn + xr);
+        if (y + 3 < p.h) rn += p.src_pitch;  // clamp at the last row
         const double dm = wmc_px64(a, b, c, l, u, r, e, f, g);
         double v;
         if (p.flow) {
@@ -144,6 +149,7 @@ __global__ void __launch_bounds__(32 * kWarps) wmc_f64_kernel(const Step64 p) {
         if (live) dst[(int64_t)y * p.dst_pitch + x] = v;
         a = l; b = u; c = r;
         l = e; u = f; r = g;
+        e = ne; f = nf; g = ng;
     }
     if (p.flag && __any_sync(0xffffffffu, bad && live) && lane == 0) atomicMin(p.flag, p.iter);
 }

@@ -29,6 +29,11 @@ CF_API int cf_device_alloc(size_t bytes, void** dptr) {
 
 CF_API int cf_device_free(void* dptr) { return st(cudaFree(dptr)); }
 
+CF_API int cf_device_memset(void* dptr, int value, size_t bytes, void* stream) {
+    if (!dptr) return CF_EINVAL;
+    return st(cudaMemsetAsync(dptr, value, bytes, (cudaStream_t)stream));
+}
+
 CF_API int cf_copy(void* dst, const void* src, size_t bytes, void* stream) {
     if (!dst || !src) return CF_EINVAL;
     return st(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));

@@ -1,0 +1,417 @@
+// paper_1903_07189_b200/csrc/wmc_map.cuh -- the WMC map (wmc_half_laplace,
+// SPEC.md:171-179) as a dedicated streaming kernel, and the map's selection
+// rule shared with the small-image flat kernel.  DESIGN.md §3.3, §4.
+//
+// One evaluation per pixel: nothing to block temporally, so the kernel is
+// built for issue efficiency rather than reuse.
+//  * A warp owns 128 contiguous columns (two 64-column chunks packed as
+//    pairs {chunk 0 col c, chunk 1 col c}: the canonical sequence runs as
+//    FFMA2 / FADD2, as in the flow kernel) and streams a strip of rows.
+//  * Rows are staged in a warp-private shared-memory ring by cp.async with
+//    CLAMPED source coordinates: window column -1 / 64 and the rows above /
+//    below the image hold the edge pixels, so the clamp-to-edge stencil
+//     needs no checked path at all -- every warp, border or not,
+//    runs the same loop.
+//  * Two output rows per step: rows y-1 .. y+2 are read once (4 row loads
+//    for 2 rows instead of 6) and the two rows' eight pixel pairs are
+//    independent work for the scheduler; the row sums l+r and (a+c)+(l+r)
+//    carry from one row to the next (bit-identical to recomputing them).
+//  * Selection by the U/S rule (map_fast below): two 8-way integer
+//    minimum trees (3-input VIMNMX3) over the D_k bit patterns and one packed
+//    add give the first-index minimum AND the opposite-sign runner-up
+//    distance the near-tie test needs -- instead of the 7-pick FSETP/FSEL
+//    tournament plus a separate 8-sum near-tie scan.  The tournament runs
+//    only for an exact opposite-sign tie (warp-uniform branch, rare).
+//  * One warp vote per 2-row step for the rare path (near ties resolved in
+//    fp64, exact opposite-sign ties by the tournament), which recomputes the
+//    flagged pairs out of line.
+#pragma once
+#include "wmc_sweep.cuh"
+
+namespace cfk {
+
+// min over 8 as 3-input trees (ptxas: VIMNMX3 / VIMNMX, 4 ops each)
+__device__ __forceinline__ uint32_t umin8(const uint32_t (&v)[8]) {
+    const uint32_t a = min(min(v[0], v[1]), v[2]);
+    const uint32_t b = min(min(v[3], v[4]), v[5]);
+    const uint32_t c = min(v[6], v[7]);
+    return min(min(a, b), c);
+}
+__device__ __forceinline__ int32_t smin8(const uint32_t (&v)[8]) {
+    const int32_t a = min(min((int32_t)v[0], (int32_t)v[1]), (int32_t)v[2]);
+    const int32_t b = min(min((int32_t)v[3], (int32_t)v[4]), (int32_t)v[5]);
+    const int32_t c = min((int32_t)v[6], (int32_t)v[7]);
+    return min(min(a, b), c);
+}
+
+// The map's selection and near-tie test (oracle/wmc_px.h
+// map_best_f32 is the same rule), per pixel:
+//   U = min_k bits(D_k) unsigned, S = min_k bits(D_k) signed;
+//   x = fl(float(U) + float(S));  b = x > 0 ? float(S) : float(U);
+//   U != S and x neither > 0 nor < 0 (exact opposite-sign tie, or NaN):
+//     b = the first-index tournament;
+//   tie iff |x| <= tau && |x| < |b|, tau = fmaf(|n12u|, 1.5*2^-19, fl(|b|*2^-20)).
+// The tie test is evaluated with the fast b: where the tournament is needed
+// x is 0 (|b| is the tied magnitude either way) or NaN (no tie either way).
+// The fast path returns b and a "rare" flag per pixel (tie, or tournament
+// needed); map_pair_fix redoes flagged pixels.
+__device__ __forceinline__ f2 map_fast(const PairD& D, bool& rare) {
+    uint32_t dl[8], dh[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        dl[k] = __float_as_uint(lo(D.d[k]));
+        dh[k] = __float_as_uint(hi(D.d[k]));
+    }
+    const uint32_t U0 = umin8(dl), U1 = umin8(dh);
+    const int32_t S0 = smin8(dl), S1 = smin8(dh);
+    const f2 x = add2(pk(__uint_as_float(U0), __uint_as_float(U1)),
+                      pk(__int_as_float(S0), __int_as_float(S1)));
+    const float x0 = lo(x), x1 = hi(x);
+    const float b0 = x0 > 0.0f ? __int_as_float(S0) : __uint_as_float(U0);
+    const float b1 = x1 > 0.0f ? __int_as_float(S1) : __uint_as_float(U1);
+    const float tau0 = __fmaf_rn(fabsf(lo(D.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b0), 0x1.0p-20f));
+    const float tau1 = __fmaf_rn(fabsf(hi(D.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b1), 0x1.0p-20f));
+    // A superset of {near tie} u {tournament needed}, two predicates a pixel:
+    // both need mixed signs (U != S; with one sign |x| = 2|b| >= |b|), and
+    // |x| <= tau (a near tie needs it; x == 0 satisfies it) or x NaN -- the
+    // unordered compare.  map_pair_fix applies the exact rule.
+    rare = ((U0 != (uint32_t)S0) & !(fabsf(x0) > tau0)) |
+           ((U1 != (uint32_t)S1) & !(fabsf(x1) > tau1));
+    return pk(b0, b1);
+}
+
+// The complete rule for one pixel of a flagged pair: tie -> the SPEC-faithful
+// fp64 evaluation, else the first-index tournament.  Recomputes D from the
+// neighbourhood with the same operands in the same order (V = a+e | b+f |
+// c+g, W = V + V', H = l+r, T = (a+c)+(l+r) -- bit-identical to the
+// streamed / carried sums).  Out of line: rare, and kept out of the loop's
+// instruction-cache footprint.
+__device__ __noinline__ f2 map_pair_fix(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f, f2 g,
+                                        f2 hw) {
+    const f2 Vl = add2(a, e), Vc = add2(b, f), Vr = add2(c, g);
+    const f2 Wm = add2(Vl, Vc), W0 = add2(Vc, Vr);
+    const f2 Hc = add2(l, r);
+    const f2 Tm = add2(add2(a, c), Hc);
+    PairD D;
+    f2 hb, t0;
+    pair_d(a, b, c, l, u, r, e, f, g, Wm, W0, Hc, Tm, hb, t0, D);
+    float h[2] = {lo(hw), hi(hw)};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        float d[8];
+        uint32_t bits[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            d[i] = k ? hi(D.d[i]) : lo(D.d[i]);
+            bits[i] = __float_as_uint(d[i]);
+        }
+        const uint32_t U = umin8(bits);
+        const int32_t S = smin8(bits);
+        const float x = __fadd_rn(__uint_as_float(U), __int_as_float(S));
+        const float bf = x > 0.0f ? __int_as_float(S) : __uint_as_float(U);
+        const float n12 = k ? hi(D.n12u) : lo(D.n12u);
+        const float tau = __fmaf_rn(fabsf(n12), 0x1.8p-19f, __fmul_rn(fabsf(bf), 0x1.0p-20f));
+        if (fabsf(x) <= tau && fabsf(x) < fabsf(bf))  // near tie: SPEC-faithful fp64
+            h[k] = k ? wmc_px_f64(hi(a), hi(b), hi(c), hi(l), hi(u), hi(r), hi(e), hi(f), hi(g))
+                     : wmc_px_f64(lo(a), lo(b), lo(c), lo(l), lo(u), lo(r), lo(e), lo(f), lo(g));
+        else if (U != (uint32_t)S && !(x > 0.0f || x < 0.0f))  // exact tie: first index
+            h[k] = __fmul_rn(select8(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7]),
+                             0x1.555556p-4f);  // fl(1/12)
+    }
+    return pk(h[0], h[1]);
+}
+
+// H^w of the map for a pixel pair (fast path), `rare` if either pixel may
+// need map_pair_fix; the row sums carried in Hc / Tm.
+__device__ __forceinline__ f2 map_pair(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f, f2 g,
+                                       f2 Wm, f2 W0, f2& Hc, f2& Tm, bool& rare) {
+    PairD D;
+    f2 hb, t0;
+    pair_d(a, b, c, l, u, r, e, f, g, Wm, W0, Hc, Tm, hb, t0, D);
+    Hc = hb;
+    Tm = t0;
+    const f2 best = map_fast(D, rare);
+    return mul2(best, kC12x2);
+}
+
+// ---- the streaming map kernel ---------------------------------------------
+// Lane i owns columns 4i .. 4i+3 of each of the warp's two 128-column chunks
+// (4 pixel pairs per row: 4 independent chains for the scheduler, and the
+// per-row costs -- ring wait, copies, loads, vote -- spread over 8 pixels).
+constexpr int kMapCols = 4;                   // columns per lane per chunk
+constexpr int kMapChunk = 32 * kMapCols;      // 128
+#ifndef CF_MAP_PD
+#define CF_MAP_PD 6
+#endif
+constexpr int kMapPD = CF_MAP_PD;             // prefetch distance (rows)
+constexpr int kMapRing = 8;                   // ring rows (>= kMapPD + 2, power of 2)
+constexpr int kMapRowBytes = 8 * (kMapChunk + 2);  // pairs for window columns -1 .. 128
+#ifndef CF_MAP_WARPS
+#define CF_MAP_WARPS 4
+#endif
+constexpr int kMapWarps = CF_MAP_WARPS;       // warps per block
+static_assert(kMapRing >= kMapPD + 2, "ring too small for the prefetch distance");
+
+struct MapParams {
+    const float* src;
+    float* dst;
+    int64_t src_pitch, src_plane, dst_pitch, dst_plane;
+    int32_t w, h, planes;
+    int32_t n_pairs;       // 256-column chunk pairs per row
+    int32_t strip_rows, n_strips;
+    int32_t st128;         // every output row 16-byte aligned
+};
+
+// the 6 pairs (window columns 4i-1 .. 4i+4) of one ring row: 3 LDS.128
+__device__ __forceinline__ void lds_row6(uint32_t a, f2 (&q)[6]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                     : "=l"(q[2 * k]), "=l"(q[2 * k + 1]) : "r"(a + 16 * k));
+}
+
+// One warp's strip.  Ring slot of row r: (r - (ys - 1)) & 7.
+// INTERIOR: every column x0-1 .. x0+256 inside the image (no clamping).
+template <bool INTERIOR>
+struct MapWarp {
+    const MapParams& p;
+    int lane, ys, ye, x0;
+    const float* src;      // plane base
+    const char* pf;        // column x0 of the next row to prefetch (row clamp(yp))
+    int yp;
+    uint32_t sbase, lofs;
+    f2 hc[4], tm[4];
+
+    __device__ __forceinline__ MapWarp(const MapParams& p_) : p(p_) {}
+
+    __device__ __forceinline__ uint32_t slot(int k) const {
+        return sbase + (uint32_t)(k & (kMapRing - 1)) * kMapRowBytes;
+    }
+    // cp.async row yp (clamped) into ring slot k, then step to the next row.
+    // The copy's lane mapping is NOT the compute mapping: copy k (0..8) of
+    // lane L fills ring word 32k + L, i.e. pair (32k + L)/2 - 1 of chunk L&1
+    // (window columns -1 .. 128 of both chunks, interleaved as pairs), so
+    // every copy instruction reads two 64-byte runs of the row and writes 128
+    // contiguous bytes of shared memory (no bank conflicts); a lane-per-
+    // column mapping read 4 lines and hit one bank 8 times per instruction.
+    __device__ __forceinline__ void prefetch_next(int k) {
+        const uint32_t s = slot(k) + 4 * lane;
+        const int c0 = lane / 2 - 1 + kMapChunk * (lane & 1);  // window column (chunk offset) of copy 0
+        if (INTERIOR) {
+            const char* g = pf + 4 * c0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) cp_async4(s + 128 * kk, g + 64 * kk);
+            if (lane < 4) cp_async4(s + 128 * 8, g + 64 * 8);
+        } else {  // image-edge warp: clamped columns
+            const float* row = reinterpret_cast<const float*>(pf);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                cp_async4(s + 128 * kk, row + min(max(x0 + c0 + 16 * kk, 0), p.w - 1));
+            if (lane < 4) cp_async4(s + 128 * 8, row + min(max(x0 + c0 + 128, 0), p.w - 1));
+        }
+        // clamp-to-edge rows: rows < 0 read row 0, rows >= h read row h-1
+        if (yp >= 0 && yp < p.h - 1) pf += p.src_pitch * 4;
+        ++yp;
+    }
+
+    // 16-byte stores (chunk 0 = lo halves at x0 + 4i .., chunk 1 = hi halves
+    // at x0 + 128 + 4i ..) where the rows are 16-byte aligned
+    __device__ __forceinline__ void store(float* row, const f2 (&nv)[kMapCols]) const {
+        if (INTERIOR && p.st128) {
+            asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row), "f"(lo(nv[0])),
+                         "f"(lo(nv[1])), "f"(lo(nv[2])), "f"(lo(nv[3])) : "memory");
+            asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + kMapChunk),
+                         "f"(hi(nv[0])), "f"(hi(nv[1])), "f"(hi(nv[2])), "f"(hi(nv[3]))
+                         : "memory");
+            return;
+        }
+#pragma unroll
+        for (int j = 0; j < kMapCols; ++j) {
+            const int xa = x0 + kMapCols * lane + j;
+            if (INTERIOR || xa < p.w) row[j] = lo(nv[j]);
+            if (INTERIOR || xa + kMapChunk < p.w) row[kMapChunk + j] = hi(nv[j]);
+        }
+    }
+
+    __device__ __forceinline__ void run(float* dst) {
+        // prologue: rows ys-1 .. ys-1+PD-1 -> slots 0 .. PD-1, a group each
+#pragma unroll
+        for (int k = 0; k < kMapPD; ++k) {
+            prefetch_next(k);
+            cp_async_commit();
+        }
+        // the first row's row sums (what it would have carried): rows ys-1, ys
+        asm volatile("cp.async.wait_group %0;" ::"n"(kMapPD - 2) : "memory");
+        __syncwarp();
+        {
+            f2 m[6], o[6];
+            lds_row6(slot(0) + lofs, m);
+            lds_row6(slot(1) + lofs, o);
+#pragma unroll
+            for (int j = 0; j < kMapCols; ++j) {
+                hc[j] = add2(o[j], o[j + 2]);
+                tm[j] = add2(add2(m[j], m[j + 2]), hc[j]);
+            }
+        }
+        float* sp = dst + (int64_t)ys * p.dst_pitch + x0 + kMapCols * lane;
+        for (int y = ys; y < ye; ++y) {
+            const int k = y - ys;  // slot of row y-1
+            // rows y-1 .. y+1 landed: of the PD + k groups issued (rows up to
+            // y+PD-2), at most PD-3 may still be pending
+            asm volatile("cp.async.wait_group %0;" ::"n"(kMapPD - 3) : "memory");
+            __syncwarp();
+            if (yp <= ye) prefetch_next(k + kMapPD);  // row y+PD-1 (the strip needs rows <= ye)
+            cp_async_commit();
+            f2 m[6], o[6], q[6];
+            lds_row6(slot(k) + lofs, m);
+            lds_row6(slot(k + 1) + lofs, o);
+            lds_row6(slot(k + 2) + lofs, q);
+            f2 V[6], W[5], out[kMapCols];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) V[i] = add2(m[i], q[i]);
+#pragma unroll
+            for (int i = 0; i < 5; ++i) W[i] = add2(V[i], V[i + 1]);
+            bool rare = false;
+#pragma unroll
+            for (int j = 0; j < kMapCols; ++j) {
+                bool r;
+#if defined(CF_MAP_EXP) && CF_MAP_EXP == 1  // diagnostic (wrong results): data movement only
+                out[j] = add2(add2(m[j + 1], q[j + 1]), W[j]);
+                r = false;
+#elif defined(CF_MAP_EXP) && CF_MAP_EXP == 2  // diagnostic (wrong results): no selection
+                {
+                    PairD D;
+                    f2 hb, t0;
+                    pair_d(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j], q[j + 1],
+                           q[j + 2], W[j], W[j + 1], hc[j], tm[j], hb, t0, D);
+                    hc[j] = hb;
+                    tm[j] = t0;
+                    out[j] = add2(add2(add2(D.d[0], D.d[1]), add2(D.d[2], D.d[3])),
+                                  add2(add2(D.d[4], D.d[5]), add2(D.d[6], D.d[7])));
+                    r = false;
+                }
+#else
+                out[j] = map_pair(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j],
+                                  q[j + 1], q[j + 2], W[j], W[j + 1], hc[j], tm[j], r);
+#endif
+                rare |= r;
+            }
+            if (__any_sync(kFull, rare)) {  // rare: near ties / exact opposite-sign ties
+                if (rare) {
+#pragma unroll
+                    for (int j = 0; j < kMapCols; ++j)
+                        out[j] = map_pair_fix(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2],
+                                              q[j], q[j + 1], q[j + 2], out[j]);
+                }
+            }
+            store(sp, out);
+            sp += p.dst_pitch;
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");  // no copy outlives the warp
+    }
+};
+
+#ifndef CF_MAP_MINB
+#define CF_MAP_MINB 3  // resident blocks per SM the register budget targets
+#endif
+__global__ void __launch_bounds__(32 * kMapWarps, CF_MAP_MINB) wmc_map_kernel(const MapParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int64_t task = (int64_t)blockIdx.x * kMapWarps + (threadIdx.x >> 5);
+    const int64_t per_plane = (int64_t)p.n_pairs * p.n_strips;
+    if (task >= per_plane * p.planes) return;  // warp-uniform
+    const int plane = (int)(task / per_plane);
+    const int64_t rest = task - (int64_t)plane * per_plane;
+    const int strip = (int)(rest / p.n_pairs);
+    const int cpair = (int)(rest - (int64_t)strip * p.n_pairs);
+    const int lane = threadIdx.x & 31;
+    const int x0 = cpair * 2 * kMapChunk;
+    const float* src = p.src + (int64_t)plane * p.src_plane;
+    float* dst = p.dst + (int64_t)plane * p.dst_plane;
+    const int ys = strip * p.strip_rows;
+    const float* row0 = src + (int64_t)max(ys - 1, 0) * p.src_pitch;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) +
+                           (uint32_t)(threadIdx.x >> 5) * (kMapRing * kMapRowBytes);
+    auto init = [&](auto& mw) {
+        mw.lane = lane;
+        mw.ys = ys;
+        mw.ye = min(ys + p.strip_rows, p.h);
+        mw.x0 = x0;
+        mw.src = src;
+        mw.yp = ys - 1;
+        mw.sbase = sbase;
+        mw.lofs = 8 * kMapCols * lane;  // window columns 4i-1 .. 4i+4
+    };
+    if (x0 > 0 && x0 + 2 * kMapChunk < p.w) {
+        MapWarp<true> mw(p);
+        init(mw);
+        mw.pf = reinterpret_cast<const char*>(row0 + x0);
+        mw.run(dst);
+    } else {
+        MapWarp<false> mw(p);
+        init(mw);
+        mw.pf = reinterpret_cast<const char*>(row0);
+        mw.run(dst);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Flat map kernel for small images: one thread per horizontal
+// pixel pair loads its clamped 3x4 neighbourhood from global memory (L1/L2
+// served) and runs map_pair with the same operands in the same order
+// (V = a+e | b+f | c+g, W = V+V', H = l+r, T = (a+c)+(l+r)), so it is
+// bit-identical to the streaming kernel.  A single small map is latency
+// bound: every pixel pair in flight at once beats warps streaming strips.
+__global__ void __launch_bounds__(256) wmc_map_flat_kernel(const float* __restrict__ src,
+                                                          float* __restrict__ dst, int32_t w,
+                                                          int32_t h, int64_t src_pitch,
+                                                          int64_t src_plane, int64_t dst_pitch,
+                                                          int64_t dst_plane, int32_t planes) {
+    const int32_t pw = (w + 1) / 2;  // pixel pairs per row
+    const int64_t n = (int64_t)pw * h * planes;
+    // grid-stride with a warp-uniform trip count (map_pair votes)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t base = blockIdx.x * (int64_t)blockDim.x;
+    for (int64_t i0 = base; i0 < n; i0 += stride) {
+        const int64_t i = min(i0 + threadIdx.x, n - 1);  // tail lanes redo the last pair
+        const bool live = i0 + threadIdx.x < n;
+        const int32_t px = (int32_t)(i % pw);
+        const int64_t r = i / pw;
+        const int32_t y = (int32_t)(r % h);
+        const int32_t pl = (int32_t)(r / h);
+        const float* plane = src + pl * src_plane;
+        const int x0 = 2 * px;
+        int cxs[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cxs[k] = min(max(x0 - 1 + k, 0), w - 1);
+        const float* rows[3] = {plane + (int64_t)max(y - 1, 0) * src_pitch,
+                                plane + (int64_t)y * src_pitch,
+                                plane + (int64_t)min(y + 1, h - 1) * src_pitch};
+        float v[3][4];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[rr][k] = __ldg(rows[rr] + cxs[k]);
+        // pair k = {column x0-1+k, column x0+k}: the neighbourhood of the pixel pair
+        f2 m[3], o[3], q[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            m[k] = pk(v[0][k], v[0][k + 1]);
+            o[k] = pk(v[1][k], v[1][k + 1]);
+            q[k] = pk(v[2][k], v[2][k + 1]);
+        }
+        const f2 V0 = add2(m[0], q[0]), V1 = add2(m[1], q[1]), V2 = add2(m[2], q[2]);
+        const f2 Wm = add2(V0, V1), W0 = add2(V1, V2);
+        f2 Hc = add2(o[0], o[2]);
+        f2 Tm = add2(add2(m[0], m[2]), Hc);
+        bool rare;
+        f2 hw = map_pair(m[0], m[1], m[2], o[0], o[1], o[2], q[0], q[1], q[2], Wm, W0, Hc, Tm, rare);
+        if (rare) hw = map_pair_fix(m[0], m[1], m[2], o[0], o[1], o[2], q[0], q[1], q[2], hw);
+        if (live) {
+            float* out = dst + pl * dst_plane + (int64_t)y * dst_pitch;
+            out[x0] = lo(hw);
+            if (x0 + 1 < w) out[x0 + 1] = hi(hw);
+        }
+    }
+}
+
+}  // namespace cfk

@@ -987,69 +987,4 @@ __global__ void __launch_bounds__(kThreads,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Flat map kernel for small images: one thread per horizontal
-// pixel pair, the 3x4 clamped neighbourhood loaded straight from global
-// memory (L1/L2-served), the same canonical sequence and near-tie rule as the
-// streaming map (pair_d / select_pair / near_tie_pair / wmc_px_f64, operands
-// in the same order: V = a+e | b+f | c+g, W = V+V', H = l+r,
-// T = (a+c)+(l+r)), so it is bit-identical to it.  A single small map is
-// latency-bound: every pixel pair in flight at once beats warps streaming
-// short strips.
-__global__ void __launch_bounds__(256) wmc_map_flat_kernel(const float* __restrict__ src,
-                                                          float* __restrict__ dst, int32_t w,
-                                                          int32_t h, int64_t src_pitch,
-                                                          int64_t src_plane, int64_t dst_pitch,
-                                                          int64_t dst_plane, int32_t planes) {
-    const int32_t pw = (w + 1) / 2;                       // pixel pairs per row
-    const int64_t n = (int64_t)pw * h * planes;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t px = (int32_t)(i % pw);
-        const int64_t r = i / pw;
-        const int32_t y = (int32_t)(r % h);
-        const int32_t pl = (int32_t)(r / h);
-        const float* plane = src + pl * src_plane;
-        const int x0 = 2 * px;
-        int cx[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) cx[k] = min(max(x0 - 1 + k, 0), w - 1);
-        const float* rows[3] = {plane + (int64_t)max(y - 1, 0) * src_pitch,
-                                plane + (int64_t)y * src_pitch,
-                                plane + (int64_t)min(y + 1, h - 1) * src_pitch};
-        float v[3][4];
-#pragma unroll
-        for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[rr][k] = __ldg(rows[rr] + cx[k]);
-        // pair k = {column x0-1+k, column x0+k}: the neighbourhood of the pixel pair
-        f2 m[3], o[3], q[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            m[k] = pk(v[0][k], v[0][k + 1]);
-            o[k] = pk(v[1][k], v[1][k + 1]);
-            q[k] = pk(v[2][k], v[2][k + 1]);
-        }
-        const f2 V0 = add2(m[0], q[0]), V1 = add2(m[1], q[1]), V2 = add2(m[2], q[2]);
-        const f2 Wm = add2(V0, V1), W0 = add2(V1, V2);
-        const f2 Hc = add2(o[0], o[2]);
-        const f2 Tm = add2(add2(m[0], m[2]), Hc);
-        PairD D;
-        f2 hb, t0;
-        pair_d(m[0], m[1], m[2], o[0], o[1], o[2], q[0], q[1], q[2], Wm, W0, Hc, Tm, hb, t0, D);
-        const f2 b = select_pair(D);
-        f2 hw = mul2(b, kC12x2);
-        bool tie0, tie1;
-        near_tie_pair(D, b, tie0, tie1);
-        float h0 = lo(hw), h1 = hi(hw);
-        if (tie0) h0 = wmc_px_f64(lo(m[0]), lo(m[1]), lo(m[2]), lo(o[0]), lo(o[1]), lo(o[2]),
-                                  lo(q[0]), lo(q[1]), lo(q[2]));
-        if (tie1) h1 = wmc_px_f64(hi(m[0]), hi(m[1]), hi(m[2]), hi(o[0]), hi(o[1]), hi(o[2]),
-                                  hi(q[0]), hi(q[1]), hi(q[2]));
-        float* out = dst + pl * dst_plane + (int64_t)y * dst_pitch;
-        out[x0] = h0;
-        if (x0 + 1 < w) out[x0 + 1] = h1;
-    }
-}
-
 }  // namespace cfk

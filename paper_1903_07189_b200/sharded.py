@@ -266,6 +266,7 @@ class IpcBandFlow:
     launch i-1 read)."""
 
     RING = 4  # events per rank; neighbours lag by at most 2 sequence numbers
+    WAIT_S = 300.0  # a neighbour silent this long has died: raise instead of hanging
 
     def __init__(self, layout: BandLayout, dist, shm_name: str, group=None):
         import ctypes as C
@@ -326,6 +327,7 @@ class IpcBandFlow:
         dist.barrier(group=group)
         self.dist, self.group = dist, group
         self.seq = 0  # launches are numbered across runs (counters only grow)
+        self.stream = None  # the stream of the last run (read / close order after it)
 
     def _row_ptr(self, base: int, buf_row0: int, y: int) -> int:
         return base + (y - buf_row0) * self.row_bytes
@@ -343,7 +345,14 @@ class IpcBandFlow:
         for side in ("up", "dn"):
             if side in self.nbr:
                 q = self.nbr[side]
+                deadline = None
                 while self.count[q["rank"]] < i:
+                    now = time.monotonic()
+                    if deadline is None:
+                        deadline = now + self.WAIT_S
+                    elif now > deadline:
+                        raise RuntimeError(f"IpcBandFlow: rank {q['rank']} did not publish "
+                                           f"launch {i} within {self.WAIT_S:.0f} s")
                     time.sleep(0)
                 self._check(self._lib.cf_stream_wait_event(stream, q["ev"][i % self.RING]),
                             "wait event")
@@ -359,8 +368,11 @@ class IpcBandFlow:
         (their halo reads end before this run's initial fill overwrites them)."""
         L, lib = self.L, self._lib
         sched = launch_schedule(iters, L.k)
+        self.stream = stream
         if not sched:
             return 0
+        # the band kernels atomicMin the first bad iteration into the flag
+        self._check(lib.cf_device_memset(self.flag, 0x7F, 4, stream), "flag reset")
         base = self.seq
         if base > 0:
             self._wait(base, stream)
@@ -392,10 +404,31 @@ class IpcBandFlow:
         self.seq = base + 1 + len(sched)
         return len(sched) % 2
 
+    def first_bad_iteration(self) -> int:
+        """Collective: the first iteration (1-based) whose iterate held a
+        non-finite value on ANY rank's band, 0 if none.
+        Synchronises the run stream."""
+        import torch
+        bad = self.C.c_int32(0)
+        rc = self._lib.cf_wmc_filter_query_nonfinite(self.flag, self.C.byref(bad), self.stream)
+        if rc not in (0, 3):
+            self._check(rc, "query flag")
+        v = torch.tensor([bad.value if bad.value > 0 else 2**31 - 1], dtype=torch.int64)
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.MIN, group=self.group)
+        return 0 if int(v.item()) == 2**31 - 1 else int(v.item())
+
+    def check_finite(self) -> None:
+        """Collective: raise FlowError naming the first bad iteration."""
+        from .curveflow import FlowError
+        bad = self.first_bad_iteration()
+        if bad:
+            raise FlowError(bad)
+
     def read(self, which: int):
         """The owned rows of bufs[which] (host float32)."""
         L = self.L
         out = self.np.empty((L.r1 - L.r0, L.w), dtype=self.np.float32)
+        self._check(self._lib.cf_stream_synchronize(self.stream), "sync")
         self._check(self._lib.cf_stream_synchronize(None), "sync")
         self._check(self._lib.cf_copy(out.ctypes.data,
                                       self._row_ptr(self.bufs[which], L.buf_row0, L.r0),
@@ -405,6 +438,7 @@ class IpcBandFlow:
 
     def close(self) -> None:
         """Collective: every rank must call it (neighbours stop writing first)."""
+        self._check(self._lib.cf_stream_synchronize(self.stream), "sync")
         self._check(self._lib.cf_stream_synchronize(None), "sync")
         self.dist.barrier(group=self.group)
         for q in self.nbr.values():

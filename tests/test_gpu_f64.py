@@ -108,7 +108,7 @@ def test_flow_f64_planes_pitch_graph_replay():
 def test_flow_f64_nonfinite_names_iteration():
     # values near the fp64 maximum overflow within a few iterations; the
     # first bad iteration must be the reference's
-    img = _img(20, 24, 11, -1e308, 1e308)
+    img = _img(20, 24, 11, -1.0, 1.0) * 1.7e308
     _, bad = _ref_flow(img, 10, 1.0)
     assert bad > 0
     with pytest.raises(cf.FlowError) as e:

@@ -1,0 +1,5 @@
+O=gpurun_out; TAG=${1:-r02d}
+timeout 600 python tools/probe_map.py > $O/probe_map_$TAG.jsonl 2>&1; echo "probe rc=$?"; cat $O/probe_map_$TAG.jsonl
+timeout 1800 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "map or golden or smoke or f64" > $O/pytest_gpu_$TAG.log 2>&1
+echo "pytest rc=$?"; tail -8 $O/pytest_gpu_$TAG.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:wmc_map_kernel -s 2 -c 1 -f -o $O/${TAG}_ncu_map python tools/ncu_target.py map 3 > $O/ncu_map_$TAG.log 2>&1; echo "ncu rc=$?"
