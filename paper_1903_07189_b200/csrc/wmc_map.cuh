@@ -86,8 +86,8 @@ __device__ __forceinline__ f2 map_fast(const PairD& D, bool& rare) {
 // c+g, W = V + V', H = l+r, T = (a+c)+(l+r) -- bit-identical to the
 // streamed / carried sums).  Out of line: rare, and kept out of the loop's
 // instruction-cache footprint.
-__device__ __noinline__ f2 map_pair_fix(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f, f2 g,
-                                        f2 hw) {
+__device__ __forceinline__ f2 map_pair_fix_inl(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f,
+                                               f2 g, f2 hw) {
     const f2 Vl = add2(a, e), Vc = add2(b, f), Vr = add2(c, g);
     const f2 Wm = add2(Vl, Vc), W0 = add2(Vc, Vr);
     const f2 Hc = add2(l, r);
@@ -119,6 +119,11 @@ __device__ __noinline__ f2 map_pair_fix(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e
                              0x1.555556p-4f);  // fl(1/12)
     }
     return pk(h[0], h[1]);
+}
+
+__device__ __noinline__ f2 map_pair_fix(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f, f2 g,
+                                        f2 hw) {
+    return map_pair_fix_inl(a, b, c, l, u, r, e, f, g, hw);
 }
 
 // H^w of the map for a pixel pair (fast path), `rare` if either pixel may

@@ -822,6 +822,10 @@ struct SweepWarp {
         __syncwarp();             // rows of step t-1 and row t visible to all lanes
         if (t + kRD < rhi(0)) {
             if ((FAST && !EDGE) || !border) {
+                // (a coalesced copy mapping -- lane L filling ring word 2 +
+                // 32k + L -- was measured here too: +8 registers, no gain at
+                // K = 2, where the sweeps, not the copies, bound the kernel;
+                // the single-sweep map uses it, csrc/wmc_map.cuh)
                 uint32_t sa;
                 if constexpr (PH >= 0) sa = ring0<PH + kRD>(g0, g1) + 8 * C * lane + 8;
                 else sa = sbase + (uint32_t)((t + kRD) & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;

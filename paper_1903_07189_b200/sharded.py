@@ -336,6 +336,8 @@ class IpcBandFlow:
         """Place the owned rows (host float32, (r1 - r0) x w) into bufs[0]."""
         arr = self.np.ascontiguousarray(band, dtype=self.np.float32)
         L = self.L
+        # the previous run's launches (on its own stream) still read bufs[0]
+        self._check(self._lib.cf_stream_synchronize(self.stream), "sync")
         self._check(self._lib.cf_copy(self._row_ptr(self.bufs[0], L.buf_row0, L.r0),
                                       arr.ctypes.data, arr.nbytes, None), "load")
         self._check(self._lib.cf_stream_synchronize(None), "sync")

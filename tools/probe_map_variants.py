@@ -15,11 +15,15 @@ import torch  # noqa: E402
 import paper_1903_07189_b200 as cf  # noqa: E402
 from paper_1903_07189_b200.configs import SUPPLEMENTAL  # noqa: E402
 
-c = SUPPLEMENTAL["cfg1_16k"]
+from paper_1903_07189_b200.configs import CONFIGS  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg1_16k"
+c = SUPPLEMENTAL.get(name) or CONFIGS[name]
 x = torch.from_numpy(cf.synth_image(c.h, c.w, c.seed(0), c.n_rects, c.n_discs, c.sigma)).cuda()
 ref = torch.empty_like(x)
 s = torch.cuda.current_stream().cuda_stream
 assert cf.lib().cf_wmc_map_f32(x.data_ptr(), ref.data_ptr(), c.w, c.h, c.w, 1, c.w * c.h, s) == 0
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 libs = [os.path.join(ROOT, "paper_1903_07189_b200", "libcurveflow_b200.so")] + sorted(
     glob.glob(os.path.join(ROOT, "tools", "variants", "lib_*.so")))
 for path in libs:
@@ -37,6 +41,7 @@ for path in libs:
         assert f(x.data_ptr(), y.data_ptr(), c.w, c.h, c.w, 1, c.w * c.h, s) == 0
     ts = []
     for _ in range(15):
+        flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         f(x.data_ptr(), y.data_ptr(), c.w, c.h, c.w, 1, c.w * c.h, s)
@@ -45,6 +50,6 @@ for path in libs:
         ts.append(e0.elapsed_time(e1))
     ms = statistics.median(ts)
     same = bool(torch.equal(y.view(torch.int32), ref.view(torch.int32)))
-    print(json.dumps({"lib": os.path.basename(path), "ms": round(ms, 4),
+    print(json.dumps({"config": name, "lib": os.path.basename(path), "ms": round(ms, 4),
                       "frac": round(c.w * c.h * 8 / ms / 1e6 / 6452.2, 4), "bitexact": same}),
           flush=True)
