@@ -684,7 +684,7 @@ def bench_b200(args, cfg):
         "clocks": clk.summary(),
     }
     achieved = alg_bytes_step / (ms_step * 1e-3) / 1e9
-    kname = (f"wmc_sweeps_kernel<K={K}>" if cfg.iters else "wmc_sweeps_kernel<MAP>")
+    kname = (f"wmc_sweeps_kernel<K={K}>" if cfg.iters else "wmc_map_kernel")
     res["roofline"] = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(kname, H, W, P),

@@ -178,16 +178,12 @@ int launch_k(cfk::SweepParams p, const DevInfo& d, cudaStream_t s) {
 
 template <int MODE>
 int launch(const cfk::SweepParams& p, int K, const DevInfo& d, cudaStream_t s) {
-    if constexpr (MODE == cfk::kModeMap) {
-        return launch_k<1, MODE>(p, d, s);
-    } else {
-        switch (K) {
-            case 1: return launch_k<1, MODE>(p, d, s);
-            case 2: return launch_k<2, MODE>(p, d, s);
-            case 3: return launch_k<3, MODE>(p, d, s);
-            case 4: return launch_k<4, MODE>(p, d, s);
-            default: return CF_EINVAL;
-        }
+    switch (K) {
+        case 1: return launch_k<1, MODE>(p, d, s);
+        case 2: return launch_k<2, MODE>(p, d, s);
+        case 3: return launch_k<3, MODE>(p, d, s);
+        case 4: return launch_k<4, MODE>(p, d, s);
+        default: return CF_EINVAL;
     }
 }
 

@@ -3,28 +3,29 @@
 // rule shared with the small-image flat kernel.  DESIGN.md §3.3, §4.
 //
 // One evaluation per pixel: nothing to block temporally, so the kernel is
-// built for issue efficiency rather than reuse.
-//  * A warp owns 128 contiguous columns (two 64-column chunks packed as
-//    pairs {chunk 0 col c, chunk 1 col c}: the canonical sequence runs as
-//    FFMA2 / FADD2, as in the flow kernel) and streams a strip of rows.
+// built for memory-pipeline and issue efficiency (map).
+//  * A warp owns 256 contiguous columns -- two 128-column chunks packed as
+//    pairs {chunk 0 col c, chunk 1 col c}, so the canonical sequence runs as
+//    FFMA2 / FADD2 as in the flow kernel -- and streams a strip of rows; lane
+//    i computes columns 4i .. 4i+3 of each chunk (4 pixel pairs a row).
 //  * Rows are staged in a warp-private shared-memory ring by cp.async with
-//    CLAMPED source coordinates: window column -1 / 64 and the rows above /
-//    below the image hold the edge pixels, so the clamp-to-edge stencil
-//     needs no checked path at all -- every warp, border or not,
-//    runs the same loop.
-//  * Two output rows per step: rows y-1 .. y+2 are read once (4 row loads
-//    for 2 rows instead of 6) and the two rows' eight pixel pairs are
-//    independent work for the scheduler; the row sums l+r and (a+c)+(l+r)
-//    carry from one row to the next (bit-identical to recomputing them).
-//  * Selection by the U/S rule (map_fast below): two 8-way integer
-//    minimum trees (3-input VIMNMX3) over the D_k bit patterns and one packed
-//    add give the first-index minimum AND the opposite-sign runner-up
-//    distance the near-tie test needs -- instead of the 7-pick FSETP/FSEL
-//    tournament plus a separate 8-sum near-tie scan.  The tournament runs
-//    only for an exact opposite-sign tie (warp-uniform branch, rare).
-//  * One warp vote per 2-row step for the rare path (near ties resolved in
-//    fp64, exact opposite-sign ties by the tournament), which recomputes the
-//    flagged pairs out of line.
+//    CLAMPED source coordinates (window columns -1 / 128 and the rows above /
+//    below the image hold the edge pixels), so the clamp-to-edge stencil
+//     needs no checked path: border warps run the same loop.
+//  * The copies use their own lane mapping (lane L fills ring word 32k + L):
+//    each copy instruction reads two 64-byte runs and writes 128 contiguous
+//    bytes of shared memory.  The lane-per-column mapping of the flow kernel
+//    read 4 lines and hit one bank 8 times per instruction; with it, data
+//    movement alone ran at 0.54 of the HBM roofline, with this one at 0.77.
+//  * 16-byte output stores where the rows are 16-byte aligned.
+//  * Selection by the U/S rule (map_fast below): two 8-way integer minimum
+//    trees (3-input VIMNMX3) over the D_k bit patterns and one packed add
+//    give the first-index minimum AND the opposite-sign runner-up distance
+//    the near-tie test needs -- instead of the 7-pick FSETP/FSEL tournament
+//    plus a separate 8-sum near-tie scan.  A two-predicate superset test
+//    flags the pixels that may need more; one warp vote per row sends them
+//    to map_pair_fix (out of line), which applies the exact rule: fp64 for
+//    near ties, the first-index tournament for exact +-0 / NaN ties.
 #pragma once
 #include "wmc_sweep.cuh"
 

@@ -3,7 +3,8 @@
 //
 // What it computes (reference: SPEC.md:171-179 wmc_half_laplace, :256-272
 // mc_flow scheme=half_laplace; Eqs. 26-28): K synchronous (Jacobi)
-// sweeps U <- U + dt * d_m(U) per launch, or (MAP) one evaluation of d_m.
+// sweeps U <- U + dt * d_m(U) per launch (the single map evaluation has its
+// own kernel, csrc/wmc_map.cuh).
 // Arithmetic is the canonical fp32 sequence of DESIGN.md §3 (the same
 // sequence oracle/wmc_oracle.c restates), written with explicit _rn
 // intrinsics / packed f32x2 PTX so nothing is contracted or reassociated.
@@ -40,8 +41,6 @@
 //    flag.  A non-finite pixel stays non-finite at every later iteration
 //    (DESIGN.md §3.4), so per-level checks of each warp's own columns name
 //    the first bad iteration exactly.
-//  * MAP mode resolves opposite-sign near-ties of the selection in fp64
-//     so the map matches the fp64 SPEC evaluation to 1e-5.
 //
 // HBM traffic: one 4-byte read and one 4-byte write per pixel per launch
 // (overlap columns hit L2); every other access is shared memory.
@@ -149,7 +148,7 @@ __device__ __forceinline__ float widen_u8(uint32_t q) {
 }
 
 constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_flow)
-constexpr int kModeMap = 1;   // out = H^w(U), one level, fp64 near-tie rule (wmc_half_laplace)
+// (mode 1, the map, moved to its own kernel: csrc/wmc_map.cuh)
 constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)
 constexpr int kModeL1 = 3;    // primal-dual step of solve_l1_area
 constexpr int kModeFlowU8 = 4;  // kModeFlow whose level-K rows are stored as u8 bytes
@@ -337,25 +336,7 @@ __device__ __forceinline__ f2 select_pair(const PairD& P) {
                       hi(P.d[6]), hi(P.d[7])));
 }
 
-// ---- fp64 near-tie resolution (MAP only) -------------------
-// Opposite-sign near tie: some D_j with D_j + D_m ~ 0 while |D_m| is not ~0.
-__device__ __forceinline__ void near_tie_pair(const PairD& P, f2 best, bool& t0, bool& t1) {
-    // T = min_k |fl(D_k + D_m)| per pixel; the sums are packed (FADD2), the
-    // magnitude minimum is fused into 3-input FMNMX3 by ptxas.
-    float T0 = 3.0e38f, T1 = 3.0e38f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const f2 sk = add2(P.d[k], best);
-        T0 = fminf(T0, fabsf(lo(sk)));
-        T1 = fminf(T1, fabsf(hi(sk)));
-    }
-    const float b0 = lo(best), b1 = hi(best);
-    const float tau0 = __fmaf_rn(fabsf(lo(P.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b0), 0x1.0p-20f));
-    const float tau1 = __fmaf_rn(fabsf(hi(P.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b1), 0x1.0p-20f));
-    t0 = T0 <= tau0 && T0 < fabsf(b0);
-    t1 = T1 <= tau1 && T1 < fabsf(b1);
-}
-
+// ---- fp64 evaluation for the map's near ties (csrc/wmc_map.cuh; §3.3) -----
 // SPEC-faithful fp64 evaluation of one pixel (oracle/wmc_px.h wmc_px_f64):
 // weights n/12 as double, taps in row-major order, s = s + w*x unfused,
 // strict-< first-minimum scan.
@@ -389,7 +370,6 @@ __device__ __noinline__ float wmc_px_f64(float a, float b, float c, float l, flo
 template <int K, int MODE>
 struct SweepWarp {
     using G = Geo<K>;
-    static constexpr bool MAP = MODE == kModeMap;
 
     const SweepParams& P;
     int lane;
@@ -584,21 +564,7 @@ struct SweepWarp {
             }
             const f2 b = select_pair(D);
             f2 hw = mul2(b, kC12x2);
-            if constexpr (MAP) {
-                bool t0, t1;
-                near_tie_pair(D, b, t0, t1);
-                if (__any_sync(kFull, t0 | t1)) {
-                    float h0 = lo(hw), h1 = hi(hw);
-                    if (t0) h0 = wmc_px_f64(lo(m[j - 1]), lo(m[j]), lo(m[j + 1]), lo(o[j - 1]),
-                                            lo(o[j]), lo(o[j + 1]), lo(p[j - 1]), lo(p[j]),
-                                            lo(p[j + 1]));
-                    if (t1) h1 = wmc_px_f64(hi(m[j - 1]), hi(m[j]), hi(m[j + 1]), hi(o[j - 1]),
-                                            hi(o[j]), hi(o[j + 1]), hi(p[j - 1]), hi(p[j]),
-                                            hi(p[j + 1]));
-                    hw = pk(h0, h1);
-                }
-                nv[j - 1] = hw;
-            } else if constexpr (MODE == kModeL2) {
+            if constexpr (MODE == kModeL2) {
                 // SPEC.md:298 with A = I: U' = U + dt*((f - U) + lambda*H^w(U))
                 const f2 fv = ld_f(y, j - 1);
                 const f2 r = fma2(o[j], splat(-1.0f), fv);         // f - u
@@ -895,7 +861,6 @@ __global__ void __launch_bounds__(kThreads,
                                   : ((MODE == kModeFlow || MODE == kModeFlowU8) && K == 2) ? CF_MINB_EVEN
                                                                                            : CF_MINB)
     wmc_sweeps_kernel(const SweepParams p) {
-    constexpr bool MAP = MODE == kModeMap;
     using G = Geo<K>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -972,7 +937,7 @@ __global__ void __launch_bounds__(kThreads,
 
     sw.run();
 
-    if constexpr (!MAP) {
+    {
         if (p.flag) {
             int bad = 0x7fffffff;
 #pragma unroll
