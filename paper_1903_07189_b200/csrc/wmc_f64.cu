@@ -43,7 +43,7 @@ extern "C" int cf_internal_graph_run(const void* key_bytes, size_t key_len, void
 
 namespace {
 
-constexpr int kStripRows = 32;   // rows per warp task
+constexpr int kStripRows = 64;   // rows per warp task
 constexpr int kWarps = 4;        // warps per block
 constexpr size_t kWsHeader = 256;
 
@@ -130,14 +130,19 @@ __global__ void __launch_bounds__(32 * kWarps) wmc_f64_kernel(const Step64 p) {
     double a = __ldg(rm + xl), b = __ldg(rm + xc), c = __ldg(rm + xr);
     double l = __ldg(r0 + xl), u = __ldg(r0 + xc), r = __ldg(r0 + xr);
     double e = __ldg(r1 + xl), f = __ldg(r1 + xc), g = __ldg(r1 + xr);
-    // software pipeline: row y+2's loads are in flight while row y computes
-    // (the DMULs otherwise wait on their own row's loads: long-scoreboard)
+    // software pipeline: rows y+2 and y+3 are in flight while row y computes
+    // (with one row ahead the DMULs still waited on their loads: ncu
+    // long-scoreboard 40 % of stall samples)
     const double* rn = row(y0 + 2);
+    double n1e = __ldg(rn + xl), n1f = __ldg(rn + xc), n1g = __ldg(rn + xr);
+    if (y0 + 2 < p.h - 1) rn += p.src_pitch;
+    double n2e = __ldg(rn + xl), n2f = __ldg(rn + xc), n2g = __ldg(rn + xr);
+    if (y0 + 3 < p.h - 1) rn += p.src_pitch;
     bool bad = false;
-#pragma unroll 3  // the window's register rotation disappears (renaming)
+#pragma unroll 2
     for (int y = y0; y < y1; ++y) {
-        const double ne = __ldg(rn + xl), nf = __ldg(rn + xc), ng = __ldg(rn + xr);
-        if (y + 3 < p.h) rn += p.src_pitch;  // clamp at the last row
+        const double n3e = __ldg(rn + xl), n3f = __ldg(rn + xc), n3g = __ldg(rn + xr);  // row y+4
+        if (y + 4 < p.h - 1) rn += p.src_pitch;  // clamp at the last row
         const double dm = wmc_px64(a, b, c, l, u, r, e, f, g);
         double v;
         if (p.flow) {
@@ -149,7 +154,9 @@ __global__ void __launch_bounds__(32 * kWarps) wmc_f64_kernel(const Step64 p) {
         if (live) dst[(int64_t)y * p.dst_pitch + x] = v;
         a = l; b = u; c = r;
         l = e; u = f; r = g;
-        e = ne; f = nf; g = ng;
+        e = n1e; f = n1f; g = n1g;
+        n1e = n2e; n1f = n2f; n1g = n2g;
+        n2e = n3e; n2f = n3f; n2g = n3g;
     }
     if (p.flag && __any_sync(0xffffffffu, bad && live) && lane == 0) atomicMin(p.flag, p.iter);
 }
