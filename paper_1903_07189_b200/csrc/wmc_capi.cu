@@ -216,8 +216,10 @@ int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
     p.src_plane = p.dst_plane = plane_stride;
     p.w = w; p.h = h; p.planes = planes;
     p.n_pairs = (w + 2 * cfk::kMapChunk - 1) / (2 * cfk::kMapChunk);
-    p.st128 = ((reinterpret_cast<uintptr_t>(out) & 15) == 0 && (pitch & 3) == 0 &&
-               (planes == 1 || (plane_stride & 3) == 0)) ? 1 : 0;
+    // 16-byte (4 columns a lane) or 8-byte (2) output stores need aligned rows
+    constexpr int kAl = cfk::kMapCols;  // elements
+    p.st128 = ((reinterpret_cast<uintptr_t>(out) & (4 * kAl - 1)) == 0 && (pitch % kAl) == 0 &&
+               (planes == 1 || (plane_stride % kAl) == 0)) ? 1 : 0;
     const int64_t slots = (int64_t)d.sms * warps;
     const int64_t cols = (int64_t)p.n_pairs * planes;
     double best_cost = 1e300;

@@ -144,8 +144,14 @@ __device__ __forceinline__ f2 map_pair(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e,
 // Lane i owns columns 4i .. 4i+3 of each of the warp's two 128-column chunks
 // (4 pixel pairs per row: 4 independent chains for the scheduler, and the
 // per-row costs -- ring wait, copies, loads, vote -- spread over 8 pixels).
-constexpr int kMapCols = 4;                   // columns per lane per chunk
+#ifndef CF_MAP_COLS
+#define CF_MAP_COLS 4
+#endif
+constexpr int kMapCols = CF_MAP_COLS;         // columns per lane per chunk (2 or 4)
+static_assert(kMapCols == 2 || kMapCols == 4, "2 or 4 columns per lane");
 constexpr int kMapChunk = 32 * kMapCols;      // 128
+constexpr int kMapNb = kMapCols + 2;          // pairs of a lane's neighbourhood row
+constexpr int kMapCopies = 2 * kMapCols;      // full 32-word copies per ring row (+ a 4-word tail)
 #ifndef CF_MAP_PD
 #define CF_MAP_PD 6
 #endif
@@ -169,9 +175,9 @@ struct MapParams {
 };
 
 // the 6 pairs (window columns 4i-1 .. 4i+4) of one ring row: 3 LDS.128
-__device__ __forceinline__ void lds_row6(uint32_t a, f2 (&q)[6]) {
+__device__ __forceinline__ void lds_row6(uint32_t a, f2 (&q)[kMapNb]) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
+    for (int k = 0; k < kMapNb / 2; ++k)
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
                      : "=l"(q[2 * k]), "=l"(q[2 * k + 1]) : "r"(a + 16 * k));
 }
@@ -206,14 +212,16 @@ struct MapWarp {
         if (INTERIOR) {
             const char* g = pf + 4 * c0;
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) cp_async4(s + 128 * kk, g + 64 * kk);
-            if (lane < 4) cp_async4(s + 128 * 8, g + 64 * 8);
+            for (int kk = 0; kk < kMapCopies; ++kk) cp_async4(s + 128 * kk, g + 64 * kk);
+            if (lane < 4) cp_async4(s + 128 * kMapCopies, g + 64 * kMapCopies);
         } else {  // image-edge warp: clamped columns
             const float* row = reinterpret_cast<const float*>(pf);
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
+            for (int kk = 0; kk < kMapCopies; ++kk)
                 cp_async4(s + 128 * kk, row + min(max(x0 + c0 + 16 * kk, 0), p.w - 1));
-            if (lane < 4) cp_async4(s + 128 * 8, row + min(max(x0 + c0 + 128, 0), p.w - 1));
+            if (lane < 4)
+                cp_async4(s + 128 * kMapCopies,
+                          row + min(max(x0 + c0 + 16 * kMapCopies, 0), p.w - 1));
         }
         // clamp-to-edge rows: rows < 0 read row 0, rows >= h read row h-1
         if (yp >= 0 && yp < p.h - 1) pf += p.src_pitch * 4;
@@ -224,11 +232,19 @@ struct MapWarp {
     // at x0 + 128 + 4i ..) where the rows are 16-byte aligned
     __device__ __forceinline__ void store(float* row, const f2 (&nv)[kMapCols]) const {
         if (INTERIOR && p.st128) {
-            asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row), "f"(lo(nv[0])),
-                         "f"(lo(nv[1])), "f"(lo(nv[2])), "f"(lo(nv[3])) : "memory");
-            asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + kMapChunk),
-                         "f"(hi(nv[0])), "f"(hi(nv[1])), "f"(hi(nv[2])), "f"(hi(nv[3]))
-                         : "memory");
+            if constexpr (kMapCols == 4) {
+                asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row),
+                             "f"(lo(nv[0])), "f"(lo(nv[1])), "f"(lo(nv[2])), "f"(lo(nv[3]))
+                             : "memory");
+                asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + kMapChunk),
+                             "f"(hi(nv[0])), "f"(hi(nv[1])), "f"(hi(nv[2])), "f"(hi(nv[3]))
+                             : "memory");
+            } else {
+                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(row), "f"(lo(nv[0])),
+                             "f"(lo(nv[1])) : "memory");
+                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(row + kMapChunk),
+                             "f"(hi(nv[0])), "f"(hi(nv[1])) : "memory");
+            }
             return;
         }
 #pragma unroll
@@ -250,7 +266,7 @@ struct MapWarp {
         asm volatile("cp.async.wait_group %0;" ::"n"(kMapPD - 2) : "memory");
         __syncwarp();
         {
-            f2 m[6], o[6];
+            f2 m[kMapNb], o[kMapNb];
             lds_row6(slot(0) + lofs, m);
             lds_row6(slot(1) + lofs, o);
 #pragma unroll
@@ -268,15 +284,15 @@ struct MapWarp {
             __syncwarp();
             if (yp <= ye) prefetch_next(k + kMapPD);  // row y+PD-1 (the strip needs rows <= ye)
             cp_async_commit();
-            f2 m[6], o[6], q[6];
+            f2 m[kMapNb], o[kMapNb], q[kMapNb];
             lds_row6(slot(k) + lofs, m);
             lds_row6(slot(k + 1) + lofs, o);
             lds_row6(slot(k + 2) + lofs, q);
-            f2 V[6], W[5], out[kMapCols];
+            f2 V[kMapNb], W[kMapNb - 1], out[kMapCols];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) V[i] = add2(m[i], q[i]);
+            for (int i = 0; i < kMapNb; ++i) V[i] = add2(m[i], q[i]);
 #pragma unroll
-            for (int i = 0; i < 5; ++i) W[i] = add2(V[i], V[i + 1]);
+            for (int i = 0; i < kMapNb - 1; ++i) W[i] = add2(V[i], V[i + 1]);
             bool rare = false;
 #pragma unroll
             for (int j = 0; j < kMapCols; ++j) {
@@ -345,7 +361,7 @@ __global__ void __launch_bounds__(32 * kMapWarps, CF_MAP_MINB) wmc_map_kernel(co
         mw.src = src;
         mw.yp = ys - 1;
         mw.sbase = sbase;
-        mw.lofs = 8 * kMapCols * lane;  // window columns 4i-1 .. 4i+4
+        mw.lofs = 8 * kMapCols * lane;  // window columns C*i-1 .. C*i+C
     };
     if (x0 > 0 && x0 + 2 * kMapChunk < p.w) {
         MapWarp<true> mw(p);
