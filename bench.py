@@ -268,11 +268,9 @@ def bench_b200(args, cfg):
     # sweeps per launch = the C-ABI filter's schedule for this geometry
     K = int(L.cf_wmc_filter_sweeps_per_launch(cfg.w, cfg.h, cfg.planes))
     if world > 1 and cfg.sharding == "rows":
-        # row bands: at N >= 8 the per-rank band is short and the per-launch
-        # fixed costs (boundary kernels, exchange, join) favour 3 sweeps per
-        # launch (tools/probe_shard_host.py: N=8 15.1 vs 16.1 ms, N=4 29.1 vs 25.7)
-        if world >= 8:
-            K = max(K, 3)
+        # row bands: the step is replayed as one CUDA graph, so launch count
+        # costs no host time and the filter's K = 2 stays (N = 8 band:
+        # 134 us per 2-sweep launch vs 210 per 3-sweep, tools/probe_shard_host.py)
         lay = sharded.BandLayout(cfg.h, cfg.w, rank, world, K)
         rows = (lay.r0, lay.r1)
     elif world > 1 and cfg.sharding == "images":

@@ -42,3 +42,31 @@ for world in (2, 4, 8):
         print(f"world={world} k={k}: launches={n} host {t_host / n * 1e6:.0f} us/launch, "
               f"gpu {e0.elapsed_time(e1) / n * 1e3:.0f} us/launch, wall {t_wall * 1e3:.1f} ms",
               flush=True)
+
+# The same step captured as one CUDA graph (what bench.py does at N > 1):
+# band kernels, the side-stream interior launches and their events replay
+# without the Python loop (P2P stubbed here: NCCL needs one GPU per rank).
+for world in (8,):
+    for k in (2, 3):
+        lay = sharded.BandLayout(H, W, 1, world, k)
+        a = torch.rand((lay.rows, W), device="cuda")
+        b = torch.empty_like(a)
+        flow = sharded.ShardedFlow(lay, sharded.cuda_compute(), NoDist(),
+                                   side_stream=torch.cuda.Stream())
+        flow.run(a, b, 20, 1.0)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            flow.run(a, b, 200, 1.0)
+        g.replay()
+        torch.cuda.synchronize()
+        n = len(sharded.launch_schedule(200, k))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        g.replay()
+        t_host = time.perf_counter() - t0
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"graph world={world} k={k}: launches={n} host {t_host / n * 1e6:.2f} us/launch, "
+              f"gpu {e0.elapsed_time(e1) / n * 1e3:.0f} us/launch", flush=True)
