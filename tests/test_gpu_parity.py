@@ -957,3 +957,51 @@ def test_u8_out_store_alignment(out_pitch, out_off):
         assert np.array_equal(got[:, :w], ref[p]), f"plane {p}"
         assert np.all(got[:, w:] == 7)           # pitch padding untouched
     assert np.all(flat[:out_off] == 7)
+
+
+def _crafted_map_image(h, w, seed):
+    """Tie-rich and extreme content for the map's selection rule (DESIGN.md
+    §3.3): dyadic step edges and checkerboards (exact opposite-sign ties),
+    signed zeros, constant patches, values that overflow the fp32 sums
+    (NaN / Inf D's), NaN / Inf pixels, and noise around them."""
+    rng = np.random.default_rng(seed)
+    img = rng.random((h, w), dtype=np.float32)
+    yy, xx = np.mgrid[0:h, 0:w]
+    q = (h // 4, w // 4)
+    img[:q[0], :q[1]] = ((xx[:q[0], :q[1]] // 3) % 2).astype(np.float32)            # stripes
+    img[:q[0], q[1]:2 * q[1]] = (((xx + yy)[:q[0], q[1]:2 * q[1]]) % 2) * 0.5         # checker
+    img[q[0]:2 * q[0], :q[1]] = (xx[q[0]:2 * q[0], :q[1]] > yy[q[0]:2 * q[0], :q[1]]) * 0.25
+    img[q[0]:2 * q[0], q[1]:2 * q[1]] = -0.0                                          # -0 patch
+    img[q[0]:2 * q[0], q[1]:2 * q[1]:3] = 0.0
+    img[2 * q[0]:2 * q[0] + 5, :] = 1.0                                               # constant band
+    s = rng.integers(0, h * w, 40)
+    img.flat[s[:10]] = 3.0e38
+    img.flat[s[10:20]] = -3.0e38
+    img.flat[s[20:27]] = np.inf
+    img.flat[s[27:33]] = -np.inf
+    img.flat[s[33:]] = np.nan
+    return img
+
+
+def _same_or_both_nan(got, ref, what):
+    g, r = np.asarray(got, np.float32), np.asarray(ref, np.float32)
+    both_nan = np.isnan(g) & np.isnan(r)
+    bad = (g.view(np.uint32) != r.view(np.uint32)) & ~both_nan
+    assert not bad.any(), f"{what}: {int(bad.sum())} mismatches, first at {np.argwhere(bad)[0]}"
+
+
+@pytest.mark.parametrize("h,w", [(64, 100), (37, 513), (768, 1000), (700, 1300)])
+def test_map_crafted_ties_and_extremes(h, w):
+    """Flat (small) and streaming (> 512 Ki px, edge and interior warps) map
+    kernels on tie-rich / extreme content: equal to the oracle's restatement
+    of the same rule bit for bit (NaN payloads aside)."""
+    img = _crafted_map_image(h, w, seed=h + w)
+    got = cf.wmc_half_laplace(torch.from_numpy(img).cuda()).cpu().numpy()
+    _same_or_both_nan(got, oracle.wmc_map_f32(img), f"crafted map {h}x{w}")
+    # finite-only variant (the fp64 near-tie rule must hold the 1e-5 contract)
+    fin = np.nan_to_num(img, nan=0.5, posinf=1.0, neginf=0.0)
+    fin = np.clip(fin, -1.0, 1.0).astype(np.float32)
+    got = cf.wmc_half_laplace(torch.from_numpy(fin).cuda()).cpu().numpy()
+    assert_bitexact(got, oracle.wmc_map_f32(fin), f"crafted finite map {h}x{w}")
+    d = np.abs(got.astype(np.float64) - oracle.wmc_map_f64(fin.astype(np.float64)))
+    assert d.max() <= 1e-5, d.max()
