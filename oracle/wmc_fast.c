@@ -8,7 +8,7 @@
  * (the scalar restatement of SPEC.md:171-179 / :256-272, PAPER.md Eqs.
  * 26-28), in the same operand order, with the same roundings:
  *   - fp32 canonical:  wmc_px_f32_full() + the flow step
- *     fmaf(dt, H^w, u) of or_flow_f32, or the map's near-tie rule
+ *     fmaf(fl(dt*fl(1/12)), D_m, u) of or_flow_f32, or the map's near-tie rule
  *     (map_best_f32 / wmc_map_px_f32);
  *   - fp64 SPEC-faithful: wmc_px_f64() (row-major taps, s = s + w*x, weights
  *     n/12 rounded once, strict-< first-minimum) + u + dt*H (or_flow_f64).
@@ -94,7 +94,7 @@ static inline float pk32(float l, float r) { return fabsf(r) < fabsf(l) ? r : l;
         DS[4] = D4; DS[5] = D5; DS[6] = D6; DS[7] = D7;                                  \
     } while (0)
 
-/* mode 0: out = fmaf(dt, H^w, u) (flow step);  mode 1: out = H^w with the
+/* mode 0: out = fmaf(fl(dt * fl(1/12)), D_m, u) (flow step);  mode 1: out = H^w with the
  * map's near-tie flag in tie[] (the caller resolves flagged pixels). */
 static void row32(const float* R0, const float* R1, const float* R2, float* O, int8_t* tie,
                   int w, int mode, float dt) {
@@ -107,7 +107,7 @@ static void row32(const float* R0, const float* R1, const float* R2, float* O, i
         px32 o;
         wmc_px_f32_full(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x], R2[xp], &o);
         if (mode == 0) {
-            O[x] = fmaf(dt, o.best * C12, R1[x]);
+            O[x] = fmaf(dt * C12, o.best, R1[x]);
         } else {
             int t;
             O[x] = map_best_f32(&o, &t) * C12;
@@ -115,13 +115,14 @@ static void row32(const float* R0, const float* R1, const float* R2, float* O, i
         }
     }
     if (mode == 0) {
+        const float dt12 = dt * C12;  /* fl(dt * fl(1/12)) */
         for (int x = 1; x < w - 1; ++x) {
             float DS[8], best, n12u;
             CANON_BEST(R0[x - 1], R0[x], R0[x + 1], R1[x - 1], R1[x], R1[x + 1], R2[x - 1], R2[x],
                        R2[x + 1], best, n12u);
             (void)n12u;
             (void)DS;
-            O[x] = fmaf(dt, best * C12, R1[x]);
+            O[x] = fmaf(dt12, best, R1[x]);
         }
     } else {
         for (int x = 1; x < w - 1; ++x) {

@@ -160,12 +160,24 @@ static inline float wmc_at_f32(const float* in, int w, int h, int64_t pitch, int
     return wmc_px_f32(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x], R2[xp]);
 }
 
+/* The selected D_m (= 12 * d_m) of the flow's canonical evaluation. */
+static inline float best_at_f32(const float* in, int w, int h, int64_t pitch, int y, int x) {
+    const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
+    const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
+    const float* R0 = in + (int64_t)ym * pitch;
+    const float* R1 = in + (int64_t)y * pitch;
+    const float* R2 = in + (int64_t)yp * pitch;
+    px32 o;
+    wmc_px_f32_full(R0[xm], R0[x], R0[xp], R1[xm], R1[x], R1[xp], R2[xm], R2[x], R2[xp], &o);
+    return o.best;
+}
+
 typedef struct {
     const float* in;
     float* out;
     int w, h;
     int64_t pitch;
-    int flow;  /* 0: map (tie rule) ; 1: out = fmaf(dt, H^w, u) ; 2: flow H^w */
+    int flow;  /* 0: map (tie rule) ; 1: out = fmaf(fl(dt*fl(1/12)), D_m, u) ; 2: flow H^w */
     float dt;
     volatile int* bad; /* per-row non-finite marker (flow only) */
     int8_t* ties;      /* map only, nullable: 1 where the fp64 tie rule fired */
@@ -176,17 +188,18 @@ static void map32_row(void* vctx, int y) {
     const float* in = c->in;
     float* o = c->out + (int64_t)y * c->pitch;
     int bad = 0;
+    const float dt12 = c->dt * C12;  /* fl(dt * fl(1/12)) */
     for (int x = 0; x < c->w; ++x) {
         int tie = 0;
-        float hw = wmc_at_f32(in, c->w, c->h, c->pitch, y, x, !c->flow, &tie);
-        if (c->ties) c->ties[(int64_t)y * c->w + x] = (int8_t)tie;
         if (c->flow == 1) {
-            float v = fmaf(c->dt, hw, in[(int64_t)y * c->pitch + x]);
+            const float v = fmaf(dt12, best_at_f32(in, c->w, c->h, c->pitch, y, x),
+                                 in[(int64_t)y * c->pitch + x]);
             if (!isfinite(v)) bad = 1;
             o[x] = v;
-        } else {
-            o[x] = hw;
+            continue;
         }
+        o[x] = wmc_at_f32(in, c->w, c->h, c->pitch, y, x, !c->flow, &tie);
+        if (c->ties) c->ties[(int64_t)y * c->w + x] = (int8_t)tie;
     }
     if (c->flow == 1 && bad) c->bad[y] = 1;
 }

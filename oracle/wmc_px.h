@@ -85,7 +85,8 @@ static inline double wmc_px_f64(const double* in, int w, int h, int64_t pitch, i
 /* n12u = fl(u * -12) is formed once and ADDED; D1..D4 of a constant image   */
 /* are exact zeros (fl(2*fl(6u)) == fl(12u)) and D1 wins the selection, so   */
 /* the map / flow of a constant is exact.  D_m selected by strict < on |D|   */
-/* scanning 1..8; H^w = fl(D_m * fl(1/12)); flow step fmaf(dt, H^w, u).       */
+/* scanning 1..8; map H^w = fl(D_m * fl(1/12)); flow step                  */
+/* fmaf(fl(dt * fl(1/12)), D_m, u) (the 1/12 folded into the step).          */
 /* ------------------------------------------------------------------------ */
 static const float C12 = 1.0f / 12.0f; /* fl(1/12) = 0x3DAAAAAB */
 

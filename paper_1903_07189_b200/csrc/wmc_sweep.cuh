@@ -588,7 +588,9 @@ struct SweepWarp {
                 odv[L][j - 1] = dn;
                 acc[L][j - 1] = fma2(nv[j - 1], kZero2, acc[L][j - 1]);
             } else {
-                nv[j - 1] = fma2(splat(P.dt), hw, o[j]);   // u + dt * H^w
+                // U' = fma(c, D_m, u), c = fl(dt * fl(1/12)): the 1/12 folded
+                // into the step (one rounding)
+                nv[j - 1] = fma2(splat(__fmul_rn(P.dt, 0x1.555556p-4f)), b, o[j]);
                 acc[L][j - 1] = fma2(nv[j - 1], kZero2, acc[L][j - 1]);
             }
         }

@@ -12,7 +12,9 @@ oracle and of the CUDA kernels:
   double(c)); for every fma in the sequence a*b is exact in double and the
   sum of two float32-range terms of the magnitudes involved is exact in
   double, so the single final rounding equals the fused one.
-* flow: 5 Jacobi iterations at dt = 1 (dt*H exact) of the fp32 sequence.
+* flow: 5 Jacobi iterations at dt = 1 of the fp32 sequence, with the step
+  U' = fma(fl(dt * fl(1/12)), D_m, u) rounded once (exact rational
+  arithmetic: that fma's sum is not always exact in double).
 
 Run:  python tests/golden/make_golden.py   (writes the .npz next to it)
 """
@@ -93,7 +95,28 @@ def map32(img):
     return out
 
 
-def flow32(img, iters):
+def fma32_exact(a, b, c):
+    """fl32(a*b + c) with ONE rounding, round-to-nearest-even, from exact
+    rational arithmetic (a*b + c is not always exact in double)."""
+    from fractions import Fraction
+    a, b, c = f32(a), f32(b), f32(c)
+    exact = Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c))
+    if exact == 0:  # RN: exact zero sums are +0 unless both addends are -0
+        p_neg = (np.signbit(a) != np.signbit(b))
+        return f32(-0.0) if (p_neg and np.signbit(c)) else f32(0.0)
+    cand = f32(float(exact))  # within one ulp of the answer
+    best, best_err = None, None
+    for v in (np.nextafter(cand, f32(-np.inf)), cand, np.nextafter(cand, f32(np.inf))):
+        err = abs(Fraction(float(v)) - exact)
+        if best is None or err < best_err or (err == best_err and
+                                               (int(v.view(np.uint32)) & 1) == 0):
+            best, best_err = v, err
+    return f32(best)
+
+
+def flow32(img, iters, dt=1.0):
+    """The canonical flow step: U' = fma(fl(dt * fl(1/12)), D_m, u)."""
+    c = f32(f32(dt) * C12)
     U = img.copy()
     for _ in range(iters):
         h, w = U.shape
@@ -101,7 +124,7 @@ def flow32(img, iters):
         for y in range(h):
             for x in range(w):
                 _, _, best = px32(nb(U, y, x))
-                V[y, x] = fma32(1.0, f32(best * C12), U[y, x])
+                V[y, x] = fma32_exact(c, best, U[y, x])
         U = V
     return U
 
