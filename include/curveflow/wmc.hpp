@@ -8,6 +8,8 @@
 //   curveflow::Image2D img = ...;                         // host, row-major
 //   auto hw  = curveflow::cuda::wmc_half_laplace(img);     // H2D, kernel, D2H
 //   auto out = curveflow::cuda::mc_flow(img, {1.0, 100});  // throws FlowError
+//   curveflow::Image2D64 ref = ...;                       // fp64, the reference's type
+//   auto same = curveflow::cuda::exact::mc_flow(ref, {1.0, 100});  // == reference CPU path
 //
 // Device-pointer overloads (curveflow::cuda::device::...) skip the copies and
 // are stream-ordered.  There is no CPU fallback.
@@ -33,6 +35,18 @@ struct Image2D {
     Image2D(int w, int h, float v = 0.0f) : width(w), height(h), data((size_t)w * h, v) {}
     float& at(int y, int x) { return data[(size_t)y * width + x]; }
     float at(int y, int x) const { return data[(size_t)y * width + x]; }
+};
+
+// SPEC.md:34-39 in the reference's own precision: fp64 images, processed by
+// curveflow::cuda::exact:: with the reference CPU path's arithmetic
+// -- results bit-identical to the reference's.
+struct Image2D64 {
+    int width = 0, height = 0;
+    std::vector<double> data;
+    Image2D64() = default;
+    Image2D64(int w, int h, double v = 0.0) : width(w), height(h), data((size_t)w * h, v) {}
+    double& at(int y, int x) { return data[(size_t)y * width + x]; }
+    double at(int y, int x) const { return data[(size_t)y * width + x]; }
 };
 
 // SPEC.md:250-253.  dt default 1.0 for half_laplace; 0 < dt <= 1.
@@ -274,6 +288,58 @@ inline Image2D mc_flow_sharded(const Image2D& img, const FlowConfig& cfg, int pa
         throw;
     }
 }
+
+// The reference's own fp64 arithmetic: wmc_half_laplace and
+// mc_flow on fp64 images, BIT-identical to the reference CPU implementation.
+namespace exact {
+namespace device {
+inline void wmc_half_laplace(const double* in, double* out, int w, int h,
+                             cudaStream_t s = nullptr) {
+    detail::check(cf_wmc_map_f64(in, out, w, h, w, 1, (int64_t)w * h, s), "wmc_half_laplace");
+}
+inline size_t flow_workspace_bytes(int w, int h) {
+    return cf_wmc_filter_f64_workspace_bytes(w, h, w, 1, (int64_t)w * h);
+}
+inline void mc_flow(double* img, int w, int h, const FlowConfig& cfg, void* workspace,
+                    size_t workspace_bytes, cudaStream_t s = nullptr) {
+    if (cfg.scheme != FlowConfig::Scheme::half_laplace)
+        throw std::invalid_argument("scheme=fd is outside this build (DESIGN.md §9)");
+    int32_t bad = 0;
+    const int st = cf_wmc_filter_f64(img, w, h, w, 1, (int64_t)w * h, cfg.iters, cfg.dt,
+                                     workspace, workspace_bytes, &bad, s);
+    if (st == CF_ENONFINITE) throw FlowError(bad);
+    detail::check(st, "mc_flow");
+}
+}  // namespace device
+
+inline Image2D64 wmc_half_laplace(const Image2D64& img, cudaStream_t s = nullptr) {
+    Image2D64 out(img.width, img.height);
+    const size_t n = img.data.size() * sizeof(double);
+    detail::DevBuf din(n), dout(n);
+    detail::cuda_check(cudaMemcpyAsync(din.p, img.data.data(), n, cudaMemcpyHostToDevice, s),
+                       "H2D");
+    device::wmc_half_laplace((const double*)din.p, (double*)dout.p, img.width, img.height, s);
+    detail::cuda_check(cudaMemcpyAsync(out.data.data(), dout.p, n, cudaMemcpyDeviceToHost, s),
+                       "D2H");
+    detail::cuda_check(cudaStreamSynchronize(s), "sync");
+    return out;
+}
+
+inline Image2D64 mc_flow(const Image2D64& img, const FlowConfig& cfg, cudaStream_t s = nullptr) {
+    Image2D64 out = img;
+    if (cfg.iters == 0) return out;
+    const size_t n = img.data.size() * sizeof(double);
+    const size_t wsb = device::flow_workspace_bytes(img.width, img.height);
+    detail::DevBuf dimg(n), ws(wsb);
+    detail::cuda_check(cudaMemcpyAsync(dimg.p, img.data.data(), n, cudaMemcpyHostToDevice, s),
+                       "H2D");
+    device::mc_flow((double*)dimg.p, img.width, img.height, cfg, ws.p, wsb, s);
+    detail::cuda_check(cudaMemcpyAsync(out.data.data(), dimg.p, n, cudaMemcpyDeviceToHost, s),
+                       "D2H");
+    detail::cuda_check(cudaStreamSynchronize(s), "sync");
+    return out;
+}
+}  // namespace exact
 
 // Per-channel processing: planes are independent.
 inline std::vector<Image2D> mc_flow(const std::vector<Image2D>& channels, const FlowConfig& cfg) {

@@ -5,7 +5,9 @@
 // :274 `flow --scheme half`, :458 `bench`) on seeded synthetic inputs
 // (PGM/PNG file I/O is out of scope):
 //
-//   curveflow_b200 op    --size H W --seed S           -> checksum of the map
+//   curveflow_b200 op    --size H W --seed S [--fp64]  -> checksum of the map
+//                                                       (--fp64: curveflow::cuda::exact, the
+//                                                        reference's own fp64 arithmetic)
 //   curveflow_b200 flow  --size H W --iters N --dt D [--parts P]
 //                                                       -> checksum of U^N (P row bands:
 //                                                          the single-process sharded filter)
@@ -28,11 +30,18 @@
 
 namespace {
 
-uint64_t fnv1a(const std::vector<float>& v) {
+template <typename T>
+uint64_t fnv1a(const std::vector<T>& v) {
     uint64_t h = 1469598103934665603ull;
     const unsigned char* p = reinterpret_cast<const unsigned char*>(v.data());
-    for (size_t i = 0; i < v.size() * sizeof(float); ++i) h = (h ^ p[i]) * 1099511628211ull;
+    for (size_t i = 0; i < v.size() * sizeof(T); ++i) h = (h ^ p[i]) * 1099511628211ull;
     return h;
+}
+
+curveflow::Image2D64 widen(const curveflow::Image2D& img) {
+    curveflow::Image2D64 out(img.width, img.height);
+    for (size_t i = 0; i < img.data.size(); ++i) out.data[i] = img.data[i];
+    return out;
 }
 
 }  // namespace
@@ -49,7 +58,7 @@ int main(int argc, char** argv) {
     uint64_t seed = 1;
     double dt = 1.0, lambda = 0.0, alpha = 1.0;
     int parts = 1;
-    bool dt_set = false;
+    bool dt_set = false, fp64 = false;
     std::string model = "l2";
     for (int i = 2; i < argc; ++i) {
         if (!std::strcmp(argv[i], "--size") && i + 2 < argc) {
@@ -70,6 +79,8 @@ int main(int argc, char** argv) {
             lambda = std::atof(argv[++i]);
         } else if (!std::strcmp(argv[i], "--alpha") && i + 1 < argc) {
             alpha = std::atof(argv[++i]);
+        } else if (!std::strcmp(argv[i], "--fp64")) {
+            fp64 = true;
         } else if (!std::strcmp(argv[i], "--reps") && i + 1 < argc) {
             reps = std::atoi(argv[++i]);
         }
@@ -77,7 +88,16 @@ int main(int argc, char** argv) {
     curveflow::Image2D img(W, H);
     if (cf_synth_f32(img.data.data(), W, H, W, seed, 20, 20, 0.1, 0) != CF_OK) return 1;
     try {
-        if (cmd == "op") {
+        if (cmd == "op" && fp64) {
+            auto m = curveflow::cuda::exact::wmc_half_laplace(widen(img));
+            std::printf("{\"op\": \"wmc\", \"fp64\": true, \"h\": %d, \"w\": %d, "
+                        "\"fnv1a\": \"%016llx\"}\n", H, W, (unsigned long long)fnv1a(m.data));
+        } else if (cmd == "flow" && fp64) {
+            auto u = curveflow::cuda::exact::mc_flow(widen(img), {dt, iters});
+            std::printf("{\"op\": \"flow\", \"fp64\": true, \"h\": %d, \"w\": %d, "
+                        "\"iters\": %d, \"fnv1a\": \"%016llx\"}\n", H, W, iters,
+                        (unsigned long long)fnv1a(u.data));
+        } else if (cmd == "op") {
             auto m = curveflow::cuda::wmc_half_laplace(img);
             std::printf("{\"op\": \"wmc\", \"h\": %d, \"w\": %d, \"fnv1a\": \"%016llx\"}\n", H, W,
                         (unsigned long long)fnv1a(m.data));

@@ -162,6 +162,21 @@ def test_cpp_cli_matches_oracle():
                                          "--iters", str(it), "--parts", str(parts)],
                                         capture_output=True, text=True, check=True).stdout)
         assert out["fnv1a"] == fnv(ref), parts
+    # the reference's own fp64 arithmetic through curveflow::cuda::exact (C++)
+    def fnv64(a):
+        h = 1469598103934665603
+        for byte in np.ascontiguousarray(a, np.float64).tobytes():
+            h = ((h ^ byte) * 1099511628211) & (2**64 - 1)
+        return f"{h:016x}"
+    img64 = img.astype(np.float64)
+    out = json.loads(subprocess.run([exe, "flow", "--size", str(H), str(W), "--seed", "3",
+                                     "--iters", str(it), "--fp64"], capture_output=True,
+                                    text=True, check=True).stdout)
+    assert out["fnv1a"] == fnv64(oracle.flow_f64(img64, it, 1.0)[0])
+    out = json.loads(subprocess.run([exe, "op", "--size", str(H), str(W), "--seed", "3",
+                                     "--fp64"], capture_output=True, text=True,
+                                    check=True).stdout)
+    assert out["fnv1a"] == fnv64(oracle.wmc_map_f64(img64))
     # smooth through curveflow::cuda::solve
     for model in ("l1", "l2"):
         out = json.loads(subprocess.run(
