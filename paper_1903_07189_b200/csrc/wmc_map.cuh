@@ -174,12 +174,28 @@ struct MapParams {
     int32_t st128;         // every output row 16-byte aligned
 };
 
-// the 6 pairs (window columns 4i-1 .. 4i+4) of one ring row: 3 LDS.128
-__device__ __forceinline__ void lds_row6(uint32_t a, f2 (&q)[kMapNb]) {
+// Ring rows are stored with their 16-byte chunks swizzled (4 columns a
+// lane): chunk q lives at q ^ ((q >> 3) & 1).  A lane's neighbourhood is
+// chunks 2i .. 2i+2 (lane stride 32 bytes), which unswizzled hit each bank
+// group twice per LDS.128 (8 shared-memory wavefronts instead of 4); the
+// swizzle spreads every 8 consecutive lanes over all 8 groups.  The copies
+// write whole 128-byte groups of 8 chunks, so they stay conflict-free.
+#ifndef CF_MAP_SWZ
+#define CF_MAP_SWZ 1
+#endif
+constexpr bool kMapSwz = CF_MAP_SWZ && kMapCols == 4;
+__host__ __device__ constexpr uint32_t map_swz_chunk(uint32_t q) {
+    return kMapSwz ? (q ^ ((q >> 3) & 1u)) : q;
+}
+
+// the kMapNb pairs (window columns C*i-1 .. C*i+C) of one ring row: one
+// LDS.128 per 16-byte chunk, at the lane's (swizzled) chunk offsets
+__device__ __forceinline__ void lds_row6(uint32_t row, const uint32_t (&co)[kMapNb / 2],
+                                         f2 (&q)[kMapNb]) {
 #pragma unroll
     for (int k = 0; k < kMapNb / 2; ++k)
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
-                     : "=l"(q[2 * k]), "=l"(q[2 * k + 1]) : "r"(a + 16 * k));
+                     : "=l"(q[2 * k]), "=l"(q[2 * k + 1]) : "r"(row + co[k]));
 }
 
 // One warp's strip.  Ring slot of row r: (r - (ys - 1)) & 7.
@@ -191,8 +207,10 @@ struct MapWarp {
     const float* src;      // plane base
     const char* pf;        // column x0 of the next row to prefetch (row clamp(yp))
     int yp;
-    uint32_t sbase, lofs;
-    f2 hc[4], tm[4];
+    uint32_t sbase;
+    uint32_t co[kMapNb / 2];   // this lane's neighbourhood chunks (byte offsets in a ring row)
+    uint32_t cpe, cpo;         // this lane's copy word offset for even / odd copies
+    f2 hc[kMapCols], tm[kMapCols];
 
     __device__ __forceinline__ MapWarp(const MapParams& p_) : p(p_) {}
 
@@ -207,20 +225,22 @@ struct MapWarp {
     // contiguous bytes of shared memory (no bank conflicts); a lane-per-
     // column mapping read 4 lines and hit one bank 8 times per instruction.
     __device__ __forceinline__ void prefetch_next(int k) {
-        const uint32_t s = slot(k) + 4 * lane;
+        const uint32_t s = slot(k);
         const int c0 = lane / 2 - 1 + kMapChunk * (lane & 1);  // window column (chunk offset) of copy 0
         if (INTERIOR) {
             const char* g = pf + 4 * c0;
 #pragma unroll
-            for (int kk = 0; kk < kMapCopies; ++kk) cp_async4(s + 128 * kk, g + 64 * kk);
-            if (lane < 4) cp_async4(s + 128 * kMapCopies, g + 64 * kMapCopies);
+            for (int kk = 0; kk < kMapCopies; ++kk)
+                cp_async4(s + 128 * kk + ((kk & 1) ? cpo : cpe), g + 64 * kk);
+            if (lane < 4) cp_async4(s + 128 * kMapCopies + cpe, g + 64 * kMapCopies);
         } else {  // image-edge warp: clamped columns
             const float* row = reinterpret_cast<const float*>(pf);
 #pragma unroll
             for (int kk = 0; kk < kMapCopies; ++kk)
-                cp_async4(s + 128 * kk, row + min(max(x0 + c0 + 16 * kk, 0), p.w - 1));
+                cp_async4(s + 128 * kk + ((kk & 1) ? cpo : cpe),
+                          row + min(max(x0 + c0 + 16 * kk, 0), p.w - 1));
             if (lane < 4)
-                cp_async4(s + 128 * kMapCopies,
+                cp_async4(s + 128 * kMapCopies + cpe,
                           row + min(max(x0 + c0 + 16 * kMapCopies, 0), p.w - 1));
         }
         // clamp-to-edge rows: rows < 0 read row 0, rows >= h read row h-1
@@ -267,8 +287,8 @@ struct MapWarp {
         __syncwarp();
         {
             f2 m[kMapNb], o[kMapNb];
-            lds_row6(slot(0) + lofs, m);
-            lds_row6(slot(1) + lofs, o);
+            lds_row6(slot(0), co, m);
+            lds_row6(slot(1), co, o);
 #pragma unroll
             for (int j = 0; j < kMapCols; ++j) {
                 hc[j] = add2(o[j], o[j + 2]);
@@ -285,9 +305,9 @@ struct MapWarp {
             if (yp <= ye) prefetch_next(k + kMapPD);  // row y+PD-1 (the strip needs rows <= ye)
             cp_async_commit();
             f2 m[kMapNb], o[kMapNb], q[kMapNb];
-            lds_row6(slot(k) + lofs, m);
-            lds_row6(slot(k + 1) + lofs, o);
-            lds_row6(slot(k + 2) + lofs, q);
+            lds_row6(slot(k), co, m);
+            lds_row6(slot(k + 1), co, o);
+            lds_row6(slot(k + 2), co, q);
             f2 V[kMapNb], W[kMapNb - 1], out[kMapCols];
 #pragma unroll
             for (int i = 0; i < kMapNb; ++i) V[i] = add2(m[i], q[i]);
@@ -361,7 +381,14 @@ __global__ void __launch_bounds__(32 * kMapWarps, CF_MAP_MINB) wmc_map_kernel(co
         mw.src = src;
         mw.yp = ys - 1;
         mw.sbase = sbase;
-        mw.lofs = 8 * kMapCols * lane;  // window columns C*i-1 .. C*i+C
+        // window columns C*i-1 .. C*i+C: 16-byte chunks C*i/2 + k (swizzled)
+#pragma unroll
+        for (int k = 0; k < kMapNb / 2; ++k)
+            mw.co[k] = 16u * map_swz_chunk((uint32_t)(kMapCols * lane / 2 + k));
+        // copy kk writes word 32kk + lane, i.e. chunk 8kk + lane/4: for odd kk
+        // the swizzle flips bit 0 of the chunk (kk even: no change)
+        mw.cpe = 16u * map_swz_chunk((uint32_t)(lane >> 2)) + 4u * (lane & 3);
+        mw.cpo = 16u * (map_swz_chunk((uint32_t)(8 + (lane >> 2))) - 8u) + 4u * (lane & 3);
     };
     if (x0 > 0 && x0 + 2 * kMapChunk < p.w) {
         MapWarp<true> mw(p);
