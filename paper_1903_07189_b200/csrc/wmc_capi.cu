@@ -194,16 +194,23 @@ int launch(const cfk::SweepParams& p, int K, const DevInfo& d, cudaStream_t s) {
 // The streaming map (csrc/wmc_map.cuh): one warp per 256 columns x strip;
 // strips sized so waves x (rows + warm-up) is minimal over the resident slots.
 int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
-               int64_t plane_stride, const DevInfo& d, cudaStream_t s) {
+               int64_t plane_stride, const DevInfo& d, cudaStream_t s,
+               double* seg_sums = nullptr, double q = 1.0, int qkind = 1) {
     constexpr size_t smem = (size_t)cfk::kMapWarps * cfk::kMapRing * cfk::kMapRowBytes;
-    static std::atomic<int> occ{-1};  // resident warps per SM (same on every B200)
+    // 0: plain map; 1..4: the fused energy epilogue for q = 1, 2, 0.5, other
+    const int qk = seg_sums == nullptr ? 0 : (qkind >= 1 && qkind <= 3 ? qkind : 4);
+    void (*const kerns[5])(cfk::MapParams) = {cfk::wmc_map_kernel<0>, cfk::wmc_map_kernel<1>,
+                                              cfk::wmc_map_kernel<2>, cfk::wmc_map_kernel<3>,
+                                              cfk::wmc_map_kernel<4>};
+    auto kern = kerns[qk];
+    static std::atomic<int> occ_cache[5] = {-1, -1, -1, -1, -1};  // warps per SM (every B200)
+    std::atomic<int>& occ = occ_cache[qk];
     int warps = occ.load(std::memory_order_acquire);
     if (warps < 0) {
         if (smem > 48 * 1024)
-            cudaFuncSetAttribute(cfk::wmc_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cfk::wmc_map_kernel,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern,
                                                           32 * cfk::kMapWarps, smem) != cudaSuccess ||
             blocks <= 0)
             blocks = 2;
@@ -215,6 +222,7 @@ int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
     p.src_pitch = p.dst_pitch = pitch;
     p.src_plane = p.dst_plane = plane_stride;
     p.w = w; p.h = h; p.planes = planes;
+    p.seg_sums = seg_sums; p.q = q; p.qkind = qkind;
     p.n_pairs = (w + 2 * cfk::kMapChunk - 1) / (2 * cfk::kMapChunk);
     // 16-byte (4 columns a lane) or 8-byte (2) output stores need aligned rows
     constexpr int kAl = cfk::kMapCols;  // elements
@@ -238,7 +246,7 @@ int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
     const int64_t tasks = cols * p.n_strips;
     const int64_t blocks = (tasks + cfk::kMapWarps - 1) / cfk::kMapWarps;
     if (blocks > INT_MAX) return CF_EINVAL;
-    cfk::wmc_map_kernel<<<(unsigned)blocks, 32 * cfk::kMapWarps, smem, s>>>(p);
+    kern<<<(unsigned)blocks, 32 * cfk::kMapWarps, smem, s>>>(p);
     CF_CUDA(cudaGetLastError());
     return CF_OK;
 }
@@ -476,6 +484,20 @@ int run_cached(int dev, const std::string& key, cudaStream_t s, Fn&& enqueue) {
 }
 
 }  // namespace
+
+// The WMC energy's segment sums computed in the streaming map kernel's
+// epilogue, without storing the map (wmc_reduce.cu).  CF_EINVAL when the
+// image is small enough for the flat map kernel (the caller then reduces a
+// stored map).  seg_sums: [ceil(w / 256)][planes * h].
+extern "C" int cf_internal_map_energy_segs(const float* in, int32_t w, int32_t h, int64_t pitch,
+                                           int32_t planes, int64_t plane_stride, double q,
+                                           int32_t qkind, double* seg_sums, void* stream) {
+    if (cfk::kMapCols != 4 || (int64_t)w * h * planes <= kFlatMapPixels) return CF_EINVAL;
+    DevInfo d;
+    if (int rc = device_info(&d)) return rc;
+    return launch_map(in, nullptr, w, h, pitch, planes, plane_stride, d, (cudaStream_t)stream,
+                      seg_sums, q, qkind);
+}
 
 // Shared with wmc_io.cu / wmc_shard.cpp; hidden (not part of the C-ABI).
 extern "C" void cf_internal_set_cuda_error(int e) { g_last_cuda = e; }

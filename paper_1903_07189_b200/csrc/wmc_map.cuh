@@ -166,7 +166,14 @@ static_assert(kMapRing >= kMapPD + 2, "ring too small for the prefetch distance"
 
 struct MapParams {
     const float* src;
-    float* dst;
+    float* dst;            // nullable with seg_sums set: the energy alone, no map stored
+    // Fused WMC energy (csrc/wmc_reduce.cu's fixed order):
+    // per row and 256-column segment, the sum of |H|^q -- lane i's columns
+    // 4i..4i+3 then 128+4i..128+4i+3 sequentially, then the xor butterfly --
+    // into seg_sums[segment * planes * h + plane * h + y].
+    double* seg_sums;      // nullable
+    double q;
+    int32_t qkind;         // 1: |H|, 2: H*H, 3: sqrt|H|, 0: pow(|H|, q)
     int64_t src_pitch, src_plane, dst_pitch, dst_plane;
     int32_t w, h, planes;
     int32_t n_pairs;       // 256-column chunk pairs per row
@@ -198,16 +205,38 @@ __device__ __forceinline__ void lds_row6(uint32_t row, const uint32_t (&co)[kMap
                      : "=l"(q[2 * k]), "=l"(q[2 * k + 1]) : "r"(row + co[k]));
 }
 
+// |H|^q in fp64 (csrc/wmc_reduce.cu term(): the same expressions); the
+// general power out of line (eight inlined pow() copies per row flooded the
+// instruction cache)
+__device__ __noinline__ double energy_pow(double a, double q) { return pow(a, q); }
+template <int QK>  // 1: |H|, 2: H*H, 3: sqrt|H|, 4: pow(|H|, q)
+__device__ __forceinline__ double energy_term(float hv, double q) {
+    const double a = fabs((double)hv);
+    if constexpr (QK == 1) return a;
+    else if constexpr (QK == 2) return __dmul_rn(a, a);
+    else if constexpr (QK == 3) return __dsqrt_rn(a);
+    else return energy_pow(a, q);
+}
+
+// The energy order's in-lane sum of the 8 terms (csrc/wmc_reduce.cu): a
+// pairwise tree, ((t0+t1)+(t2+t3)) + ((t4+t5)+(t6+t7)) -- depth 3.
+__device__ __forceinline__ double lane_tree8(const double (&t)[8]) {
+    return __dadd_rn(__dadd_rn(__dadd_rn(t[0], t[1]), __dadd_rn(t[2], t[3])),
+                     __dadd_rn(__dadd_rn(t[4], t[5]), __dadd_rn(t[6], t[7])));
+}
+
 // One warp's strip.  Ring slot of row r: (r - (ys - 1)) & 7.
 // INTERIOR: every column x0-1 .. x0+256 inside the image (no clamping).
-template <bool INTERIOR>
+template <bool INTERIOR, int QK>  // QK > 0: the fused energy epilogue of that power
 struct MapWarp {
+    static constexpr bool ENERGY = QK > 0;
     const MapParams& p;
     int lane, ys, ye, x0;
     const float* src;      // plane base
     const char* pf;        // column x0 of the next row to prefetch (row clamp(yp))
     int yp;
     uint32_t sbase;
+    int64_t plane_row0;        // plane * h (the energy's row index base)
     uint32_t co[kMapNb / 2];   // this lane's neighbourhood chunks (byte offsets in a ring row)
     uint32_t cpe, cpo;         // this lane's copy word offset for even / odd copies
     f2 hc[kMapCols], tm[kMapCols];
@@ -295,7 +324,7 @@ struct MapWarp {
                 tm[j] = add2(add2(m[j], m[j + 2]), hc[j]);
             }
         }
-        float* sp = dst + (int64_t)ys * p.dst_pitch + x0 + kMapCols * lane;
+        float* sp = dst ? dst + (int64_t)ys * p.dst_pitch + x0 + kMapCols * lane : nullptr;
         for (int y = ys; y < ye; ++y) {
             const int k = y - ys;  // slot of row y-1
             // rows y-1 .. y+1 landed: of the PD + k groups issued (rows up to
@@ -346,8 +375,28 @@ struct MapWarp {
                                               q[j], q[j + 1], q[j + 2], out[j]);
                 }
             }
-            store(sp, out);
-            sp += p.dst_pitch;
+            if constexpr (ENERGY) {  // the energy's segment sum of this row
+                double t[2 * kMapCols];
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int j = 0; j < kMapCols; ++j) {
+                        const int xa = x0 + kMapCols * lane + kMapChunk * c + j;
+                        const float hv = c ? hi(out[j]) : lo(out[j]);
+                        t[kMapCols * c + j] =
+                            (INTERIOR || xa < p.w) ? energy_term<QK>(hv, p.q) : 0.0;
+                    }
+                double acc = lane_tree8(t);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, o));
+                if (lane == 0)
+                    p.seg_sums[(int64_t)(x0 / (2 * kMapChunk)) * p.planes * p.h + plane_row0 + y] =
+                        acc;
+            }
+            if (!ENERGY || p.dst) {
+                store(sp, out);
+                sp += p.dst_pitch;
+            }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");  // no copy outlives the warp
     }
@@ -356,7 +405,14 @@ struct MapWarp {
 #ifndef CF_MAP_MINB
 #define CF_MAP_MINB 3  // resident blocks per SM the register budget targets
 #endif
-__global__ void __launch_bounds__(32 * kMapWarps, CF_MAP_MINB) wmc_map_kernel(const MapParams p) {
+#ifndef CF_MAP_MINB_ENERGY
+#define CF_MAP_MINB_ENERGY CF_MAP_MINB
+#endif
+// QK > 0: the fused energy epilogue (p.seg_sums; 1: |H|, 2: H*H, 3: sqrt,
+// 4: pow), the map store then optional (p.dst nullable)
+template <int QK>
+__global__ void __launch_bounds__(32 * kMapWarps, QK ? CF_MAP_MINB_ENERGY : CF_MAP_MINB)
+    wmc_map_kernel(const MapParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t task = (int64_t)blockIdx.x * kMapWarps + (threadIdx.x >> 5);
     const int64_t per_plane = (int64_t)p.n_pairs * p.n_strips;
@@ -368,13 +424,14 @@ __global__ void __launch_bounds__(32 * kMapWarps, CF_MAP_MINB) wmc_map_kernel(co
     const int lane = threadIdx.x & 31;
     const int x0 = cpair * 2 * kMapChunk;
     const float* src = p.src + (int64_t)plane * p.src_plane;
-    float* dst = p.dst + (int64_t)plane * p.dst_plane;
+    float* dst = p.dst ? p.dst + (int64_t)plane * p.dst_plane : nullptr;
     const int ys = strip * p.strip_rows;
     const float* row0 = src + (int64_t)max(ys - 1, 0) * p.src_pitch;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                            (uint32_t)(threadIdx.x >> 5) * (kMapRing * kMapRowBytes);
     auto init = [&](auto& mw) {
         mw.lane = lane;
+        mw.plane_row0 = (int64_t)plane * p.h;
         mw.ys = ys;
         mw.ye = min(ys + p.strip_rows, p.h);
         mw.x0 = x0;
@@ -391,12 +448,12 @@ __global__ void __launch_bounds__(32 * kMapWarps, CF_MAP_MINB) wmc_map_kernel(co
         mw.cpo = 16u * (map_swz_chunk((uint32_t)(8 + (lane >> 2))) - 8u) + 4u * (lane & 3);
     };
     if (x0 > 0 && x0 + 2 * kMapChunk < p.w) {
-        MapWarp<true> mw(p);
+        MapWarp<true, QK> mw(p);
         init(mw);
         mw.pf = reinterpret_cast<const char*>(row0 + x0);
         mw.run(dst);
     } else {
-        MapWarp<false> mw(p);
+        MapWarp<false, QK> mw(p);
         init(mw);
         mw.pf = reinterpret_cast<const char*>(row0);
         mw.run(dst);

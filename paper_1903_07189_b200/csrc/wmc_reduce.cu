@@ -10,12 +10,19 @@
 //  * corpus_stats histograms wmc_half_laplace values with bins of width 1
 //    over [-256, 256]; counts are integers.
 //
-// Fixed order used here (and restated by the oracle, bit-exact):
-//  per plane, per row y: the row is cut into 32-column blocks; a block's
-//  terms |H|^q (fp64) are combined by the butterfly tree of a warp xor-
-//  shuffle reduction (offsets 16, 8, 4, 2, 1, lane order fixed); a row sum is
-//  the sequential sum of its block sums in x order; the plane's energy is the
-//  sequential sum of its row sums in y order, and planes add in plane order.
+// Fixed order of the ENERGY (round 2; restated by the oracle, bit-exact) --
+// the map kernel's own layout (csrc/wmc_map.cuh), so the reduction can run
+// as the map's epilogue:
+//  per plane, per row y: the row is cut into 256-column segments; lane i of
+//  a segment owns columns 4i .. 4i+3 and 128+4i .. 128+4i+3, terms t0..t7 in
+//  that order (|H|^q in fp64; columns past w give 0), summed as the tree
+//  ((t0+t1)+(t2+t3)) + ((t4+t5)+(t6+t7)); the 32 lane sums combine by the
+//  butterfly tree of a warp xor-shuffle reduction (offsets 16, 8, 4, 2, 1);
+//  a row sum is the sequential sum of its segment sums in x order (from 0);
+//  the plane's energy is the sequential sum of its row sums in y order, and
+//  planes add in plane order.
+// The FIDELITY sums keep round 1's order: 32-column blocks (butterfly), block
+// sums sequential in x, rows sequential.
 //  q = 1 -> |H|, q = 2 -> H*H, q = 0.5 -> sqrt(|H|) (correctly rounded, so
 //  bit-exact); any other q uses pow() (documented 1e-12 relative tolerance).
 // The map itself is cf_wmc_map_f32 (fp32, fp64 near-tie rule).
@@ -26,6 +33,9 @@
 #include "../../include/curveflow/capi.h"
 
 extern "C" void cf_internal_set_cuda_error(int e);  // wmc_capi.cu (not exported)
+extern "C" int cf_internal_map_energy_segs(const float* in, int32_t w, int32_t h, int64_t pitch,
+                                           int32_t planes, int64_t plane_stride, double q,
+                                           int32_t qkind, double* seg_sums, void* stream);
 
 namespace {
 
@@ -90,14 +100,61 @@ __global__ void row_energy_kernel(const float* __restrict__ map, int32_t w, int3
     if (lane == 0) row_sums[row] = acc;
 }
 
-// Ordered combine of the row sums (one thread: h*planes sequential adds).
-__global__ void ordered_sum_kernel(const double* __restrict__ row_sums, int64_t n,
-                                   double* __restrict__ out) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        double s = 0.0;
-        for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, row_sums[i]);
-        *out = s;
+// One warp per (row, 256-column segment) of a dense map: the energy order's
+// segment sum (lane sums, then the xor butterfly), written by lane 0.
+__global__ void seg_energy_kernel(const float* __restrict__ map, int32_t w, int32_t h,
+                                  int64_t pitch, int32_t planes, int64_t plane_stride, double q,
+                                  int qkind, int32_t nseg, double* __restrict__ seg_sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (task >= (int64_t)h * planes * nseg) return;
+    const int64_t row = task / nseg;
+    const int s = (int)(task - row * nseg);
+    const int64_t p = row / h, y = row % h;
+    const float* r = map + p * plane_stride + y * pitch;
+    const int x0 = 256 * s + 4 * lane;
+    double t[8];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int x = x0 + 128 * c + j;
+            t[4 * c + j] = x < w ? term(r[x], q, qkind) : 0.0;
+        }
+    double acc = __dadd_rn(__dadd_rn(__dadd_rn(t[0], t[1]), __dadd_rn(t[2], t[3])),
+                           __dadd_rn(__dadd_rn(t[4], t[5]), __dadd_rn(t[6], t[7])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, o));
+    if (lane == 0) seg_sums[(int64_t)s * h * planes + row] = acc;  // [segment][row]
+}
+
+// Row sums: the segment sums of each row added in x order (one thread a
+// row; segment sums stored [segment][row], so every step reads coalesced).
+__global__ void row_from_segs_kernel(const double* __restrict__ seg_sums, int32_t nseg,
+                                     int64_t nrows, double* __restrict__ row_sums) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= nrows) return;
+    double acc = 0.0;
+    for (int i = 0; i < nseg; ++i) acc = __dadd_rn(acc, seg_sums[(int64_t)i * nrows + row]);
+    row_sums[row] = acc;
+}
+
+// Ordered combine of the row sums: h*planes sequential adds by one thread,
+// the operands staged through shared memory by the whole block (the adds are
+// a dependent chain; the loads are not, so they must not sit in it).
+__global__ void __launch_bounds__(1024) ordered_sum_kernel(const double* __restrict__ row_sums,
+                                                           int64_t n, double* __restrict__ out) {
+    __shared__ double buf[4096];
+    double s = 0.0;
+    for (int64_t base = 0; base < n; base += 4096) {
+        const int m = n - base < 4096 ? (int)(n - base) : 4096;
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) buf[i] = row_sums[base + i];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < m; ++i) s = __dadd_rn(s, buf[i]);
     }
+    if (threadIdx.x == 0) *out = s;
 }
 
 __global__ void histogram_kernel(const float* __restrict__ map, int32_t w, int32_t h,
@@ -135,7 +192,10 @@ extern "C" {
 CF_API size_t cf_wmc_reduce_workspace_bytes(int32_t w, int32_t h, int32_t planes) {
     if (w <= 0 || h <= 0 || planes <= 0) return 0;
     const size_t map = (((size_t)w * h * planes * sizeof(float)) + 255) & ~(size_t)255;
-    return map + (size_t)h * planes * sizeof(double) + 256;
+    const size_t nseg = ((size_t)w + 255) / 256;
+    // map | row sums | segment sums
+    return map + (((size_t)h * planes * sizeof(double) + 255) & ~(size_t)255) +
+           (size_t)h * planes * nseg * sizeof(double) + 256;
 }
 
 CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pitch,
@@ -150,16 +210,28 @@ CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pit
     float* map = reinterpret_cast<float*>(workspace);
     const size_t map_bytes = (((size_t)w * h * planes * sizeof(float)) + 255) & ~(size_t)255;
     double* rows = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + map_bytes);
-    // dense copy of the map (pitch = w) so the layout is independent of the input's
-    for (int p = 0; p < planes; ++p) {
-        int rc = cf_wmc_map_f32(img + p * plane_stride, map + (int64_t)p * w * h, w, h, pitch, 1,
-                                (int64_t)w * h, stream);
-        if (rc) return rc;
-    }
     const int64_t nrows = (int64_t)h * planes;
-    row_energy_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(
-        map, w, h, w, planes, (int64_t)w * h, q, qkind_of(q), rows);
-    ordered_sum_kernel<<<1, 32, 0, s>>>(rows, nrows, d_out);
+    const int32_t nseg = (w + 255) / 256;
+    double* segs = reinterpret_cast<double*>(
+        reinterpret_cast<char*>(rows) + ((nrows * sizeof(double) + 255) & ~(size_t)255));
+    // large images: the segment sums come straight out of the map kernel's
+    // epilogue (no map stored or re-read); small ones: map, then reduce it
+    const int fused = cf_internal_map_energy_segs(img, w, h, pitch, planes, plane_stride, q,
+                                                  qkind_of(q), segs, stream);
+    if (fused != CF_OK && fused != CF_EINVAL) return fused;
+    if (fused == CF_EINVAL) {
+        // dense copy of the map (pitch = w) so the layout is independent of the input's
+        for (int p = 0; p < planes; ++p) {
+            int rc = cf_wmc_map_f32(img + p * plane_stride, map + (int64_t)p * w * h, w, h, pitch,
+                                    1, (int64_t)w * h, stream);
+            if (rc) return rc;
+        }
+        const int64_t tasks = nrows * nseg;
+        seg_energy_kernel<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(
+            map, w, h, w, planes, (int64_t)w * h, q, qkind_of(q), nseg, segs);
+    }
+    row_from_segs_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(segs, nseg, nrows, rows);
+    ordered_sum_kernel<<<1, 1024, 0, s>>>(rows, nrows, d_out);
     return fail();
 }
 
@@ -177,7 +249,7 @@ CF_API int cf_wmc_fidelity_f64(const float* u, const float* f, int32_t w, int32_
     const int64_t nrows = (int64_t)h * planes;
     row_fidelity_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(
         u, f, w, h, pitch, planes, plane_stride, q, qkind_of(q), rows);
-    ordered_sum_kernel<<<1, 32, 0, s>>>(rows, nrows, d_out);
+    ordered_sum_kernel<<<1, 1024, 0, s>>>(rows, nrows, d_out);
     return fail();
 }
 

@@ -335,6 +335,23 @@ def test_wmc_energy_bitexact(q):
     assert got == oracle.wmc_energy(img, q)
 
 
+@pytest.mark.parametrize("q", [1.0, 2.0, 0.5, 1.3])
+@pytest.mark.parametrize("P,h,w", [(1, 700, 1300), (2, 520, 777), (1, 1030, 520)])
+def test_wmc_energy_fused_large(q, P, h, w):
+    """Images above the flat-kernel size: the energy's segment sums come out
+    of the streaming map kernel's epilogue (no map stored); same fixed order,
+    so bit-exact against the oracle (q = 1.3: pow, 1e-12 relative)."""
+    img = np.stack([cf.synth_image(h, w, seed=90 + s, n_rects=9, n_discs=9, sigma=0.1)
+                    for s in range(P)])
+    img = img[0] if P == 1 else img
+    got = cf.wmc_energy(torch.from_numpy(img).cuda(), q)
+    ref = oracle.wmc_energy(img, q)
+    if q == 1.3:
+        assert abs(got - ref) <= 1e-12 * ref
+    else:
+        assert got == ref
+
+
 def test_wmc_energy_general_q_and_histogram():
     img = cf.synth_image(90, 130, seed=77, n_rects=5, n_discs=5, sigma=0.1)
     d = torch.from_numpy(img).cuda()
