@@ -26,6 +26,8 @@
 //  q = 1 -> |H|, q = 2 -> H*H, q = 0.5 -> sqrt(|H|) (correctly rounded, so
 //  bit-exact); any other q uses pow() (documented 1e-12 relative tolerance).
 // The map itself is cf_wmc_map_f32 (fp32, fp64 near-tie rule).
+#include <algorithm>
+#include <climits>
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -157,6 +159,50 @@ __global__ void __launch_bounds__(1024) ordered_sum_kernel(const double* __restr
     if (threadIdx.x == 0) *out = s;
 }
 
+// bin = floor((v*scale - lo) / width), out-of-range -> clamped ends, NaN -> 0
+__device__ __forceinline__ int hist_bin(float v, float scale, float lo, float width, int nbins) {
+    const float d = __fsub_rn(__fmul_rn(v, scale), lo);
+    const float t = width == 1.0f ? d : __fdiv_rn(d, width);  // x / 1 == x exactly
+    int b = (t != t) ? 0 : (int)floorf(fminf(fmaxf(t, -1.0f), (float)nbins));
+    return min(max(b, 0), nbins - 1);
+}
+
+// Warp-private histograms in shared memory (32-bit counts, one per warp when
+// they fit, else one per block); the block's counts then go to the global
+// 64-bit counts.  Rows are walked whole
+// (coalesced loads, no per-element division).  WMC values pile into a few
+// bins, so global atomics per element serialised on them: 52 ms for 16384^2.
+__global__ void histogram_smem_kernel(const float* __restrict__ map, int32_t w, int32_t h,
+                                      int64_t pitch, int32_t planes, int64_t plane_stride,
+                                      float scale, float lo, float width, int32_t nbins,
+                                      unsigned long long* __restrict__ counts) {
+    extern __shared__ unsigned int shm[];
+    // one sub-histogram per warp when they fit (no contention between the
+    // warps on the hot bins), else one per block
+    const int nsub = (int)(blockDim.x >> 5) * nbins <= 12288 ? (int)(blockDim.x >> 5) : 1;
+    for (int i = threadIdx.x; i < nsub * nbins; i += blockDim.x) shm[i] = 0u;
+    __syncthreads();
+    unsigned int* sh = shm + (nsub > 1 ? (threadIdx.x >> 5) * nbins : 0);
+    const int64_t rows = (int64_t)h * planes;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t p = r / h, y = r - p * h;
+        const float* row = map + p * plane_stride + y * pitch;
+        for (int x0 = 0; x0 < w; x0 += blockDim.x) {  // warp-uniform trip count
+            const int x = x0 + (int)threadIdx.x;
+            const bool live = x < w;
+            // (merging same-bin lanes with __match_any_sync first cost more than
+            // the shared atomics it saves: 1.90 vs 1.08 ms for 16384^2)
+            if (live) atomicAdd(&sh[hist_bin(row[x], scale, lo, width, nbins)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) {
+        unsigned long long c = 0;
+        for (int k = 0; k < nsub; ++k) c += shm[k * nbins + i];
+        if (c) atomicAdd(counts + i, c);
+    }
+}
+
 __global__ void histogram_kernel(const float* __restrict__ map, int32_t w, int32_t h,
                                  int64_t pitch, int32_t planes, int64_t plane_stride, float scale,
                                  float lo, float width, int32_t nbins,
@@ -166,11 +212,7 @@ __global__ void histogram_kernel(const float* __restrict__ map, int32_t w, int32
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = i / ((int64_t)w * h), rem = i % ((int64_t)w * h);
         const float v = map[p * plane_stride + (rem / w) * pitch + rem % w];
-        // bin = floor((v*scale - lo) / width), out-of-range -> clamped ends
-        const float t = __fdiv_rn(__fsub_rn(__fmul_rn(v, scale), lo), width);
-        int b = (t != t) ? 0 : (int)floorf(fminf(fmaxf(t, -1.0f), (float)nbins));
-        b = min(max(b, 0), nbins - 1);
-        atomicAdd(counts + b, 1ull);
+        atomicAdd(counts + hist_bin(v, scale, lo, width, nbins), 1ull);
     }
 }
 
@@ -270,8 +312,20 @@ CF_API int cf_wmc_histogram(const float* img, int32_t w, int32_t h, int64_t pitc
         if (rc) return rc;
     }
     if (cudaMemsetAsync(d_counts, 0, sizeof(uint64_t) * nbins, s) != cudaSuccess) return fail();
-    histogram_kernel<<<1184, 256, 0, s>>>(map, w, h, w, planes, (int64_t)w * h, scale, lo, width,
-                                          nbins, reinterpret_cast<unsigned long long*>(d_counts));
+    auto* c64 = reinterpret_cast<unsigned long long*>(d_counts);
+    const int64_t rows = (int64_t)h * planes;
+    // shared-memory path: up to 12288 bins (48 KB) and fewer than 2^32
+    // pixels per block (the 32-bit shared counts cannot overflow)
+    const int blocks = (int)std::min<int64_t>(rows, 148 * 8);
+    const int64_t per_block = ((rows + blocks - 1) / blocks) * (int64_t)w;
+    if (nbins <= 12288 && per_block < (int64_t)UINT32_MAX) {
+        const size_t shb = (size_t)(8 * nbins <= 12288 ? 8 : 1) * nbins * sizeof(unsigned);
+        histogram_smem_kernel<<<blocks, 256, shb, s>>>(
+            map, w, h, w, planes, (int64_t)w * h, scale, lo, width, nbins, c64);
+    } else {
+        histogram_kernel<<<1184, 256, 0, s>>>(map, w, h, w, planes, (int64_t)w * h, scale, lo,
+                                              width, nbins, c64);
+    }
     return fail();
 }
 

@@ -352,6 +352,20 @@ def test_wmc_energy_fused_large(q, P, h, w):
         assert got == ref
 
 
+@pytest.mark.parametrize("nbins,scale,lo,width", [(512, 255.0, -256.0, 1.0),
+                                                  (7, 1000.0, -3.0, 1.0),
+                                                  (12288, 4096.0, -6144.0, 1.0),
+                                                  (20000, 4096.0, -10000.0, 1.0)])
+def test_wmc_histogram_large(nbins, scale, lo, width):
+    """Block-private shared-memory counts merged per warp (<= 12288 bins) and
+    the global-atomic fallback (more bins): exact counts on a large image."""
+    img = cf.synth_image(1000, 1300, seed=31, n_rects=9, n_discs=9, sigma=0.1)
+    d = torch.from_numpy(img).cuda()
+    got = cf.wmc_histogram(d, scale=scale, lo=lo, width=width, nbins=nbins)
+    assert np.array_equal(got, oracle.wmc_histogram(img, scale, lo, width, nbins))
+    assert int(got.sum()) == img.size
+
+
 def test_wmc_energy_general_q_and_histogram():
     img = cf.synth_image(90, 130, seed=77, n_rects=5, n_discs=5, sigma=0.1)
     d = torch.from_numpy(img).cuda()
