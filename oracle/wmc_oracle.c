@@ -457,23 +457,31 @@ OR_EXPORT double or_energy_from_map(const float* map, int32_t w, int32_t h, int3
 }
 
 /* Fidelity sum |u - f|^q (f NULL: sum |u|^q) over pitched planes, the
- * difference in fp64, in the fidelity's fixed order (32-column butterfly
- * blocks, blocks and rows sequential: wmc_reduce.cu row_fidelity_kernel). */
+ * difference in fp64, in the energy's fixed order (wmc_reduce.cu). */
 OR_EXPORT double or_fidelity(const float* u, const float* f, int32_t w, int32_t h, int64_t pitch,
                              int32_t planes, int64_t plane_stride, double q, int32_t qkind) {
+    /* the energy's order (or_energy_from_map) with terms |u - f|^q */
     double total = 0.0;
     for (int p = 0; p < planes; ++p)
         for (int y = 0; y < h; ++y) {
             const int64_t off = (int64_t)p * plane_stride + (int64_t)y * pitch;
             double row = 0.0;
-            for (int x0 = 0; x0 < w; x0 += 32) {
+            for (int x0 = 0; x0 < w; x0 += 256) {
                 double v[32];
                 for (int l = 0; l < 32; ++l) {
-                    const int x = x0 + l;
-                    if (x >= w) { v[l] = 0.0; continue; }
-                    const double a =
-                        fabs(f ? (double)u[off + x] - (double)f[off + x] : (double)u[off + x]);
-                    v[l] = qkind == 1 ? a : (qkind == 2 ? a * a : (qkind == 3 ? sqrt(a) : pow(a, q)));
+                    double t[8];
+                    for (int c = 0; c < 2; ++c)
+                        for (int j = 0; j < 4; ++j) {
+                            const int x = x0 + 4 * l + 128 * c + j;
+                            double tv = 0.0;
+                            if (x < w) {
+                                const double a = fabs(f ? (double)u[off + x] - (double)f[off + x]
+                                                        : (double)u[off + x]);
+                                tv = qkind == 1 ? a : (qkind == 2 ? a * a : (qkind == 3 ? sqrt(a) : pow(a, q)));
+                            }
+                            t[4 * c + j] = tv;
+                        }
+                    v[l] = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
                 }
                 for (int o = 16; o > 0; o >>= 1) {
                     double nv[32];

@@ -21,8 +21,8 @@
 //  a row sum is the sequential sum of its segment sums in x order (from 0);
 //  the plane's energy is the sequential sum of its row sums in y order, and
 //  planes add in plane order.
-// The FIDELITY sums keep round 1's order: 32-column blocks (butterfly), block
-// sums sequential in x, rows sequential.
+// The FIDELITY sums (SolveReport series) use the same order with terms
+// |u - f|^q, the difference taken in fp64.
 //  q = 1 -> |H|, q = 2 -> H*H, q = 0.5 -> sqrt(|H|) (correctly rounded, so
 //  bit-exact); any other q uses pow() (documented 1e-12 relative tolerance).
 // The map itself is cf_wmc_map_f32 (fp32, fp64 near-tie rule).
@@ -56,64 +56,22 @@ __device__ __forceinline__ double term(float hw, double q, int qkind) {
     return term_abs(fabs((double)hw), q, qkind);
 }
 
-// One warp per row of |u - f|^q (f nullable), same block order as the energy.
-__global__ void row_fidelity_kernel(const float* __restrict__ u, const float* __restrict__ f,
-                                    int32_t w, int32_t h, int64_t pitch, int32_t planes,
-                                    int64_t plane_stride, double q, int qkind,
-                                    double* __restrict__ row_sums) {
-    const int lane = threadIdx.x & 31;
-    const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (row >= (int64_t)h * planes) return;
-    const int64_t p = row / h, y = row % h;
-    const int64_t off = p * plane_stride + y * pitch;
-    double acc = 0.0;
-    for (int x0 = 0; x0 < w; x0 += 32) {
-        const int x = x0 + lane;
-        double v = 0.0;
-        if (x < w) {
-            const double a = f ? __dsub_rn((double)u[off + x], (double)f[off + x])
-                               : (double)u[off + x];
-            v = term_abs(fabs(a), q, qkind);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
-        acc = __dadd_rn(acc, v);
-    }
-    if (lane == 0) row_sums[row] = acc;
-}
-
-// One warp per row: block sums by xor butterfly, sequential over blocks.
-__global__ void row_energy_kernel(const float* __restrict__ map, int32_t w, int32_t h,
-                                  int64_t pitch, int32_t planes, int64_t plane_stride, double q,
-                                  int qkind, double* __restrict__ row_sums) {
-    const int lane = threadIdx.x & 31;
-    const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (row >= (int64_t)h * planes) return;
-    const int64_t p = row / h, y = row % h;
-    const float* r = map + p * plane_stride + y * pitch;
-    double acc = 0.0;
-    for (int x0 = 0; x0 < w; x0 += 32) {
-        const int x = x0 + lane;
-        double v = x < w ? term(r[x], q, qkind) : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
-        acc = __dadd_rn(acc, v);  // every lane holds the same block sum
-    }
-    if (lane == 0) row_sums[row] = acc;
-}
-
-// One warp per (row, 256-column segment) of a dense map: the energy order's
-// segment sum (lane sums, then the xor butterfly), written by lane 0.
-__global__ void seg_energy_kernel(const float* __restrict__ map, int32_t w, int32_t h,
-                                  int64_t pitch, int32_t planes, int64_t plane_stride, double q,
-                                  int qkind, int32_t nseg, double* __restrict__ seg_sums) {
+// One warp per (row, 256-column segment): the reduction order's segment sum
+// (lane terms as a pairwise tree, then the xor butterfly), written by lane 0
+// into seg_sums[segment][row].  Terms: |map|^q, or (fidelity, f2 set or not)
+// |u - f|^q with the difference in fp64.
+__global__ void seg_sum_kernel(const float* __restrict__ map, const float* __restrict__ f2,
+                               bool fid, int32_t w, int32_t h, int64_t pitch, int32_t planes,
+                               int64_t plane_stride, double q, int qkind, int32_t nseg,
+                               double* __restrict__ seg_sums) {
     const int lane = threadIdx.x & 31;
     const int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
     if (task >= (int64_t)h * planes * nseg) return;
     const int64_t row = task / nseg;
     const int s = (int)(task - row * nseg);
     const int64_t p = row / h, y = row % h;
-    const float* r = map + p * plane_stride + y * pitch;
+    const int64_t off = p * plane_stride + y * pitch;
+    const float* r = map + off;
     const int x0 = 256 * s + 4 * lane;
     double t[8];
 #pragma unroll
@@ -121,7 +79,16 @@ __global__ void seg_energy_kernel(const float* __restrict__ map, int32_t w, int3
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int x = x0 + 128 * c + j;
-            t[4 * c + j] = x < w ? term(r[x], q, qkind) : 0.0;
+            double v = 0.0;
+            if (x < w) {
+                if (fid) {
+                    const double a = f2 ? __dsub_rn((double)r[x], (double)f2[off + x]) : (double)r[x];
+                    v = term_abs(fabs(a), q, qkind);
+                } else {
+                    v = term(r[x], q, qkind);
+                }
+            }
+            t[4 * c + j] = v;
         }
     double acc = __dadd_rn(__dadd_rn(__dadd_rn(t[0], t[1]), __dadd_rn(t[2], t[3])),
                            __dadd_rn(__dadd_rn(t[4], t[5]), __dadd_rn(t[6], t[7])));
@@ -269,8 +236,8 @@ CF_API int cf_wmc_energy_f64(const float* img, int32_t w, int32_t h, int64_t pit
             if (rc) return rc;
         }
         const int64_t tasks = nrows * nseg;
-        seg_energy_kernel<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(
-            map, w, h, w, planes, (int64_t)w * h, q, qkind_of(q), nseg, segs);
+        seg_sum_kernel<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(
+            map, nullptr, false, w, h, w, planes, (int64_t)w * h, q, qkind_of(q), nseg, segs);
     }
     row_from_segs_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(segs, nseg, nrows, rows);
     ordered_sum_kernel<<<1, 1024, 0, s>>>(rows, nrows, d_out);
@@ -289,8 +256,13 @@ CF_API int cf_wmc_fidelity_f64(const float* u, const float* f, int32_t w, int32_
     cudaStream_t s = (cudaStream_t)stream;
     double* rows = reinterpret_cast<double*>(workspace);
     const int64_t nrows = (int64_t)h * planes;
-    row_fidelity_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(
-        u, f, w, h, pitch, planes, plane_stride, q, qkind_of(q), rows);
+    const int32_t nseg = (w + 255) / 256;
+    double* segs = reinterpret_cast<double*>(
+        reinterpret_cast<char*>(rows) + ((nrows * sizeof(double) + 255) & ~(size_t)255));
+    const int64_t tasks = nrows * nseg;
+    seg_sum_kernel<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(
+        u, f, true, w, h, pitch, planes, plane_stride, q, qkind_of(q), nseg, segs);
+    row_from_segs_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(segs, nseg, nrows, rows);
     ordered_sum_kernel<<<1, 1024, 0, s>>>(rows, nrows, d_out);
     return fail();
 }

@@ -46,5 +46,8 @@ nbins = 512
 counts = torch.empty(nbins, dtype=torch.int64, device="cuda")
 ms_hist = t(lambda: L.cf_wmc_histogram(x.data_ptr(), W, H, W, 1, W * H, 255.0, -256.0, 1.0, nbins,
                                        counts.data_ptr(), ws.data_ptr(), nb, s))
+ms_fid = t(lambda: L.cf_wmc_fidelity_f64(x.data_ptr(), y.data_ptr(), W, H, W, 1, W * H, 2.0,
+                                         out.data_ptr(), ws.data_ptr(), nb, s))
+print(json.dumps({"fidelity_q2_ms": round(ms_fid, 4)}))
 print(json.dumps({"map_ms": round(ms_map, 4), "energy_q1_ms": round(res[1.0], 4),
                   "energy_q2_ms": round(res[2.0], 4), "histogram_ms": round(ms_hist, 4)}))
