@@ -657,7 +657,7 @@ def bench_b200(args, cfg):
             ms = float(t.item())
         return ms / steps
 
-    # streaming steady state: enough steps for ~1.5 s of streaming (at least
+    # streaming steady state: enough steps for ~3 s of streaming (at least
     # max(8, K), at most 2000) so the pipeline fill (first H2D) and drain
     # (last D2H) are amortised like in a long-running frame pipeline; the
     # per-step estimate comes from timed warm-up steps
@@ -665,7 +665,7 @@ def bench_b200(args, cfg):
         e2e_step()
     torch.cuda.synchronize(dev)
     est_ms = e2e_timed(2)
-    e2e_steps = int(min(2000, max(8, args.steps, math.ceil(1500.0 / max(est_ms, 1e-3)))))
+    e2e_steps = int(min(2000, max(8, args.steps, math.ceil(3000.0 / max(est_ms, 1e-3)))))
     if world > 1:  # every rank runs the same count
         t = torch.tensor([e2e_steps], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
@@ -717,7 +717,7 @@ def bench_b200(args, cfg):
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4), "steps": e2e_steps,
                 "pipeline": ("H2D/D2H from pinned host memory every step on two copy streams, "
                              "triple-buffered against the compute stream; steady state over "
-                             "~1.5 s of streaming" if pipelined else
+                             "~3 s of streaming" if pipelined else
                              "H2D/D2H of each rank's band on two copy streams through "
                              "double-buffered device staging")},
         "gpu_launches": launches_per_step * args.steps,
