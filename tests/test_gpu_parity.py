@@ -1051,3 +1051,64 @@ def test_map_crafted_ties_and_extremes(h, w):
     assert_bitexact(got, oracle.wmc_map_f32(fin), f"crafted finite map {h}x{w}")
     d = np.abs(got.astype(np.float64) - oracle.wmc_map_f64(fin.astype(np.float64)))
     assert d.max() <= 1e-5, d.max()
+
+
+@pytest.mark.parametrize("P,h,w,pitch,gap", [(1, 37, 65, 72, 0), (2, 45, 77, 80, 3 * 80),
+                                             (1, 700, 1000, 1003, 0), (2, 520, 1300, 1304, 5),
+                                             (3, 333, 777, 781, 17)])
+def test_map_guard_bands(P, h, w, pitch, gap):
+    """C-ABI map (flat kernel for small, streaming kernel for large images)
+    into a pitched, plane-gapped output filled with a sentinel: the image
+    region equals the oracle bit for bit and no other byte is written."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    plane = pitch * h + gap
+    imgs = np.stack([cf.synth_image(h, w, seed=3 * P + s, n_rects=5, n_discs=5, sigma=0.1)
+                     for s in range(P)])
+    sentinel = np.uint32(0x7FBADBAD)
+    src = torch.full((P * plane + 64,), float("nan"), dtype=torch.float32, device="cuda")
+    out = torch.from_numpy(np.full(P * plane + 64, sentinel, dtype=np.uint32)).cuda()
+    for p in range(P):
+        v = src[p * plane:p * plane + h * pitch].view(h, pitch)
+        v[:, :w] = torch.from_numpy(imgs[p]).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.cf_wmc_map_f32(src.data_ptr(), out.data_ptr(), w, h, pitch, P, plane, s) == 0
+    o = out.cpu().numpy()
+    ref = oracle.wmc_map_f32(imgs if P > 1 else imgs[0])
+    ref = ref if P > 1 else ref[None]
+    mask = np.zeros(o.size, dtype=bool)
+    for p in range(P):
+        rows = o[p * plane:p * plane + h * pitch].reshape(h, pitch)
+        assert np.array_equal(rows[:, :w], ref[p].view(np.uint32)), f"plane {p}"
+        for y in range(h):
+            mask[p * plane + y * pitch:p * plane + y * pitch + w] = True
+    assert np.all(o[~mask] == sentinel), "map wrote outside the image region"
+
+
+@pytest.mark.parametrize("h,w,pitch,iters", [(37, 65, 70, 3), (300, 500, 509, 4)])
+def test_f64_guard_bands(h, w, pitch, iters):
+    """fp64 map and filter into pitched buffers: bit-exact vs the fp64
+    reference path, nothing written outside the image rows."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    img = np.random.default_rng(h).random((h, w))
+    sentinel = np.uint64(0x7FF4BADBADBADBAD)
+    s = torch.cuda.current_stream().cuda_stream
+    src = torch.from_numpy(np.full(h * pitch + 8, sentinel, dtype=np.uint64)).cuda()
+    sv = src[:h * pitch].view(torch.float64).view(h, pitch)
+    sv[:, :w] = torch.from_numpy(img).cuda()
+    out = torch.from_numpy(np.full(h * pitch + 8, sentinel, dtype=np.uint64)).cuda()
+    assert L.cf_wmc_map_f64(src.data_ptr(), out.data_ptr(), w, h, pitch, 1, h * pitch, s) == 0
+    o = out.cpu().numpy()
+    rows = o[:h * pitch].reshape(h, pitch)
+    assert np.array_equal(rows[:, :w], oracle.wmc_map_f64(img).view(np.uint64))
+    assert np.all(rows[:, w:] == sentinel) and np.all(o[h * pitch:] == sentinel)
+    nb = int(L.cf_wmc_filter_f64_workspace_bytes(w, h, pitch, 1, h * pitch))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bad = C.c_int32(0)
+    assert L.cf_wmc_filter_f64(src.data_ptr(), w, h, pitch, 1, h * pitch, iters, 1.0,
+                               ws.data_ptr(), nb, C.byref(bad), s) == 0
+    o = src.cpu().numpy()
+    rows = o[:h * pitch].reshape(h, pitch)
+    assert np.array_equal(rows[:, :w], oracle.flow_f64(img, iters, 1.0)[0].view(np.uint64))
+    assert np.all(rows[:, w:] == sentinel) and np.all(o[h * pitch:] == sentinel)
