@@ -156,7 +156,10 @@ constexpr int kMapCopies = 2 * kMapCols;      // full 32-word copies per ring ro
 #define CF_MAP_PD 6
 #endif
 constexpr int kMapPD = CF_MAP_PD;             // prefetch distance (rows)
-constexpr int kMapRing = 8;                   // ring rows (>= kMapPD + 2, power of 2)
+#ifndef CF_MAP_RING
+#define CF_MAP_RING 8
+#endif
+constexpr int kMapRing = CF_MAP_RING;         // ring rows (>= kMapPD + 2, power of 2)
 constexpr int kMapRowBytes = 8 * (kMapChunk + 2);  // pairs for window columns -1 .. 128
 #ifndef CF_MAP_WARPS
 #define CF_MAP_WARPS 4
