@@ -222,6 +222,11 @@ CF_API int32_t cf_wmc_max_sweeps_per_launch(void);
 /* geometry-dependent schedule needs no ABI change -- currently 2).          */
 CF_API int32_t cf_wmc_filter_launches(int32_t w, int32_t h, int32_t planes, int32_t iters);
 CF_API int32_t cf_wmc_filter_sweeps_per_launch(int32_t w, int32_t h, int32_t planes);
+/* 1 if the u8 entry points (_u8_f32, _u8_u8, _u8_f64 excluded) read these  */
+/* u8 rows inside the first sweep launch (4-byte aligned rows, w % 4 == 0,  */
+/* iters > 0), 0 if they run a separate widening launch first.             */
+CF_API int32_t cf_wmc_filter_u8_fused(const void* in, int64_t in_pitch, int64_t in_plane_stride,
+                                      int32_t w, int32_t iters);
 CF_API int cf_wmc_sweeps_band_f32(const float* src, int32_t src_row0, int32_t src_rows,
                                   float* dst, int32_t dst_row0, int32_t w, int32_t h,
                                   int64_t pitch, int32_t y0, int32_t y1, int32_t sweeps,

@@ -34,6 +34,7 @@ SIGNATURES = {
     "cf_last_cuda_error": (C.c_int, []),
     "cf_wmc_map_f32": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _i64, _vp]),
     "cf_wmc_filter_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32, _i64]),
+    "cf_wmc_filter_u8_fused": (_i32, [_vp, _i64, _i64, _i32, _i32]),
     "cf_wmc_filter_f32": (C.c_int, [_vp, _i32, _i32, _i64, _i32, _i64, _i32, _f32, _vp, _sz,
                                     _pi32, _vp]),
     "cf_wmc_filter_query_nonfinite": (C.c_int, [_vp, _pi32, _vp]),

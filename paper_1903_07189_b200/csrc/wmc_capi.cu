@@ -547,6 +547,12 @@ CF_API int32_t cf_wmc_filter_launches(int32_t w, int32_t h, int32_t planes, int3
     return (int32_t)schedule(iters, flow_levels(w, h, planes)).size();
 }
 
+static bool u8_fusable(const void* src0, int64_t pitch, int64_t plane, int32_t w);
+CF_API int32_t cf_wmc_filter_u8_fused(const void* in, int64_t in_pitch, int64_t in_plane_stride,
+                                      int32_t w, int32_t iters) {
+    return iters > 0 && in && w > 0 && u8_fusable(in, in_pitch, in_plane_stride, w) ? 1 : 0;
+}
+
 CF_API void cf_kernel_bank_x12(int32_t* out72) {
     // PAPER.md:411-444; SPEC.md:96-111 -- h_i * 12, [i][row][col]
     static const int32_t H12[72] = {
@@ -595,6 +601,18 @@ struct DataTerm {            // solve_l2_area / solve_l1_area (f != nullptr)
     float alpha = 1.0f;
 };
 
+// The first launch can read u8 rows itself (cfk::kModeFlowU8In) when every
+// row starts on a 4-byte boundary and holds whole 4-byte words.
+// CF_U8_FUSE=0 forces the separate widening pass (A/B measurements).
+static bool u8_fusable(const void* src0, int64_t pitch, int64_t plane, int32_t w) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("CF_U8_FUSE");
+        return !(e && e[0] == '0');
+    }();
+    return enabled && w % 4 == 0 &&
+           ((reinterpret_cast<uintptr_t>(src0) | (uintptr_t)pitch | (uintptr_t)plane) & 3) == 0;
+}
+
 struct Out8 {               // fused save-time quantisation of the last launch
     uint8_t* p = nullptr;
     int64_t pitch = 0, plane = 0;
@@ -618,13 +636,18 @@ static int enqueue_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_
     float* nxt = ws;
     float* dcur = dterm.d;      // kModeL1: follows the same ping-pong as U
     float* dnxt = dterm.d_ws;
+    // u8 input: widened inside the first launch's row loads
+    // when the bytes allow 4-byte copies, else by a separate pass
+    const bool fuse8 =
+        src_u8 && !ks.empty() && u8_fusable(src0, src_pitch, src_plane, w) && !dterm.f;
     if (src_u8) {
-        // widen u8 -> fp32 into whichever buffer makes the
-        // final launch land in `out`
+        // the widened image (or the first launch's output) goes to whichever
+        // buffer makes the final launch land in `out`
         if (ks.size() % 2 == 1) std::swap(cur, nxt);
-        if (int rc = launch_widen(static_cast<const uint8_t*>(src0), src_pitch, src_plane, cur,
-                                  pitch, plane_stride, w, h, planes, d.sms, s))
-            return rc;
+        if (!fuse8)
+            if (int rc = launch_widen(static_cast<const uint8_t*>(src0), src_pitch, src_plane, cur,
+                                      pitch, plane_stride, w, h, planes, d.sms, s))
+                return rc;
     }
     int iter = 0;
     for (size_t i = 0; i < ks.size(); ++i) {
@@ -641,10 +664,17 @@ static int enqueue_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_
         if (out8.p && i + 1 == ks.size()) {  // last launch: u8 bytes instead of fp32
             p.dst8 = out8.p; p.dst8_pitch = out8.pitch; p.dst8_plane = out8.plane;
         }
-        const int rc = dterm.d   ? launch<cfk::kModeL1>(p, ks[i], d, s)
-                       : dterm.f ? launch<cfk::kModeL2>(p, ks[i], d, s)
-                       : p.dst8  ? launch<cfk::kModeFlowU8>(p, ks[i], d, s)
-                                 : launch<cfk::kModeFlow>(p, ks[i], d, s);
+        const bool in8 = fuse8 && i == 0;    // first launch: u8 rows in
+        if (in8) {
+            p.src8 = static_cast<const uint8_t*>(src0);
+            p.src8_pitch = src_pitch; p.src8_plane = src_plane;
+        }
+        const int rc = dterm.d          ? launch<cfk::kModeL1>(p, ks[i], d, s)
+                       : dterm.f        ? launch<cfk::kModeL2>(p, ks[i], d, s)
+                       : in8 && p.dst8  ? launch<cfk::kModeFlowU8InOut>(p, ks[i], d, s)
+                       : in8            ? launch<cfk::kModeFlowU8In>(p, ks[i], d, s)
+                       : p.dst8         ? launch<cfk::kModeFlowU8>(p, ks[i], d, s)
+                                        : launch<cfk::kModeFlow>(p, ks[i], d, s);
         if (rc) return rc;
         iter += ks[i];
         std::swap(cur, nxt);

@@ -116,6 +116,12 @@ struct SweepParams {
     // instead of fp32 to dst.
     uint8_t* dst8;
     int64_t dst8_pitch, dst8_plane;
+    // Fused load-time widening (kModeFlowU8In / kModeFlowU8InOut, the u8
+    // paths' first launch): level-0 rows come from u8 bytes at src8 (global
+    // row src_row0 of plane 0) instead of src.  Host contract: src8, pitch
+    // and plane stride multiples of 4 bytes, w a multiple of 4.
+    const uint8_t* src8;
+    int64_t src8_pitch, src8_plane;
     // MODE == kModeL2 (solve_l2_area): data term f and lambda
     const float* fdata;       // global row 0 of plane 0 (same column geometry as src)
     int64_t f_pitch, f_plane; // elements
@@ -152,6 +158,16 @@ constexpr int kModeFlow = 0;  // U' = U + dt * H^w(U)                      (mc_f
 constexpr int kModeL2 = 2;    // U' = U + dt * ((f - U) + lambda * H^w(U))  (solve_l2_area)
 constexpr int kModeL1 = 3;    // primal-dual step of solve_l1_area
 constexpr int kModeFlowU8 = 4;  // kModeFlow whose level-K rows are stored as u8 bytes
+#ifndef CF_U8_EARLY
+// 1: widen row t+1 at the end of step t, off the wait -> __syncwarp path
+// (measured on cfg5: 0.2 % slower than widening row t in place at step t)
+#define CF_U8_EARLY 0
+#endif
+constexpr int kModeFlowU8In = 5;     // kModeFlow whose level-0 rows are read as u8 bytes
+constexpr int kModeFlowU8InOut = 6;  // both (a u8 -> u8 filter done in one launch)
+__host__ __device__ constexpr bool mode_u8_in(int m) { return m == kModeFlowU8In || m == kModeFlowU8InOut; }
+__host__ __device__ constexpr bool mode_u8_out(int m) { return m == kModeFlowU8 || m == kModeFlowU8InOut; }
+__host__ __device__ constexpr bool mode_flow(int m) { return m == kModeFlow || mode_u8_in(m) || mode_u8_out(m); }
 
 // Column geometry for K levels: each chunk window overlaps its neighbours by
 // A = K columns per side (the trapezoid shrinks one column per level).
@@ -259,6 +275,9 @@ __device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_rd() {
     asm volatile("cp.async.wait_group %0;" ::"n"(kRD - 1) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_rd1() {  // one row further: t + 1
+    asm volatile("cp.async.wait_group %0;" ::"n"(kRD - 2) : "memory");
 }
 // The C+2 pairs (columns C*i-1 .. C*i+C) a lane needs from one row, read
 // with 16-byte LDS from byte a = row + 8*C*i (16-aligned).
@@ -389,6 +408,10 @@ struct SweepWarp {
     const float* dsp;             // plane base of d^t (kModeL1)
     float* ddp;                   // plane base of d^{t+K} (kModeL1)
     uint8_t* d8p;                 // plane base of the u8 output (fused quantisation)
+    const uint8_t* s8p;           // plane base of the u8 input (fused widening)
+    uint32_t sel8[2];             // byte_perm selectors: chunk h's C input bytes from its words
+    int o8[2][2];                 // byte offsets in a u8 row of chunk h's staged words
+    uint32_t pend8[4];            // staged words of row t + 1, widened at the end of step t
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
     uint32_t fbase;               // this lane's slice of the data-term ring (solver modes)
@@ -431,6 +454,18 @@ struct SweepWarp {
     // cp.async this lane's 4 input values of row y into ring slot y % kRS:
     // column c of chunk h lands at byte 8*(c+1) + 4*h of the row.
     __device__ __forceinline__ void prefetch(int y) const {
+        if constexpr (kU8In) {
+            // u8 input: the 2 aligned words holding chunk h's C bytes,
+            // clamped to the row, land in this lane's region at k8Stage;
+            // widen8() turns them into the fp32 pairs at step y.
+            const uint8_t* row8 = s8p + (int64_t)(y - P.src_row0) * P.src8_pitch;
+            const uint32_t s = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane + k8Stage;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int k = 0; k < kNW8; ++k) cp_async4(s + 4 * kNW8 * h + 4 * k, row8 + o8[h][k]);
+            return;
+        }
         const float* row = srcp + (int64_t)(y - P.src_row0) * P.src_pitch;
         const uint32_t s = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane + 8;
         const float* frow = nullptr;
@@ -455,6 +490,53 @@ struct SweepWarp {
                 cp_async4(ds, drow + x0);
                 cp_async4(ds + 4, drow + x1);
             }
+        }
+    }
+
+    static constexpr bool kU8In = mode_u8_in(MODE);
+    // Words per chunk and lane: a lane's C columns start at xf = chunk * S
+    // - K + C * lane, so with C = 2 and K even they sit in one aligned word.
+    static constexpr int kNW8 = (C == 2 && K % 2 == 0) ? 1 : 2;
+    // staged words (2 * kNW8 of them) inside the lane's 8*C-byte region at
+    // +8, aligned to their total size (C = 4: at +16)
+    static constexpr int k8Stage = C == 4 ? 16 : 8;
+
+    // kU8In: this lane's staged words of row y (landed: after the wait)
+    __device__ __forceinline__ void load8(int y, uint32_t (&wd)[4]) const {
+        const uint32_t a = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane + k8Stage;
+        if constexpr (kNW8 == 1) {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wd[0]), "=r"(wd[2]) : "r"(a));
+            wd[1] = wd[0]; wd[3] = wd[2];
+        } else if constexpr (C == 4) {
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(wd[0]), "=r"(wd[1]), "=r"(wd[2]), "=r"(wd[3]) : "r"(a));
+        } else {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wd[0]), "=r"(wd[1]) : "r"(a));
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wd[2]), "=r"(wd[3]) : "r"(a + 8));
+        }
+    }
+    __device__ __forceinline__ void widen8(int y) const {
+        uint32_t wd[4];
+        load8(y, wd);
+        cvt8(y, wd);
+    }
+    // ... widened in place into its C fp32 column pairs, fl(q / 255)
+    // exactly as widen_u8 (before the __syncwarp that publishes row y)
+    __device__ __forceinline__ void cvt8(int y, const uint32_t (&wd)[4]) const {
+        const uint32_t a = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane;
+        const uint32_t q0 = __byte_perm(wd[0], wd[1], sel8[0]);
+        const uint32_t q1 = __byte_perm(wd[2], wd[3], sel8[1]);
+        const f2 two23 = pk(-8388608.0f, -8388608.0f);  // -2^23
+        const f2 inv = pk(0x1.010102p-8f, 0x1.010102p-8f);  // fl(1/255)
+        const f2 m255 = pk(-255.0f, -255.0f);
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            // 0x4B0000qq = 2^23 + q exactly
+            const float lo = __uint_as_float(__byte_perm(q0, 0x4b000000u, 0x7440u | j));
+            const float hi = __uint_as_float(__byte_perm(q1, 0x4b000000u, 0x7440u | j));
+            const f2 qf = add2(pk(lo, hi), two23);
+            const f2 r0 = mul2(qf, inv);   // multi-use: never contracted
+            sts_pair(a + 8 + 8 * j, fma2(fma2(r0, m255, qf), inv, r0));
         }
     }
 
@@ -657,7 +739,7 @@ struct SweepWarp {
                     drow[xf[1] + j] = hi(odv[K][j]);
             }
         }
-        if constexpr (L == K && MODE == kModeFlowU8) {  // quantise in the store
+        if constexpr (L == K && mode_u8_out(MODE)) {  // quantise in the store
             store_row8<!(CHECKED || EDGE)>(d8p + (int64_t)(y - P.dst_row0) * P.dst8_pitch, nv);
             return;
         }
@@ -786,10 +868,23 @@ struct SweepWarp {
     template <bool FAST, int PH = -1, bool EDGE = false>
     __device__ __forceinline__ void step(int t, const float*& lptr, float*& sptr,
                                          uint32_t g0 = 0, uint32_t g1 = 0) {
-        cp_async_wait_rd();       // this lane's copies of row t landed
+        if constexpr (kU8In && CF_U8_EARLY) {
+            // row t was widened at the end of step t-1 (the first row here);
+            // row t+1's words are read now, widened after this step's levels
+            cp_async_wait_rd1();
+            if (t == rlo(0)) widen8(t);
+            if (t + 1 < rhi(0)) load8(t + 1, pend8);
+        } else {
+            cp_async_wait_rd();       // this lane's copies of row t landed
+            if constexpr (kU8In) {
+                if (t < rhi(0)) widen8(t);
+            }
+        }
         __syncwarp();             // rows of step t-1 and row t visible to all lanes
         if (t + kRD < rhi(0)) {
-            if ((FAST && !EDGE) || !border) {
+            if constexpr (kU8In) {
+                prefetch(t + kRD);   // first launch only: the generic form is enough
+            } else if ((FAST && !EDGE) || !border) {
                 // (a coalesced copy mapping -- lane L filling ring word 2 +
                 // 32k + L -- was measured here too: +8 registers, no gain at
                 // K = 2, where the sweeps, not the copies, bound the kernel;
@@ -851,6 +946,9 @@ struct SweepWarp {
             store<1, true>(t, R4, sptr);
             shift_duals();
         }
+        if constexpr (kU8In && CF_U8_EARLY) {
+            if (t + 1 < rhi(0)) cvt8(t + 1, pend8);
+        }
         sptr += P.dst_pitch;
     }
 };
@@ -860,7 +958,7 @@ template <int K, int MODE>
 // no spills at the filter's K = 2.
 __global__ void __launch_bounds__(kThreads,
                                   (MODE == kModeL2 || MODE == kModeL1)                    ? 3
-                                  : ((MODE == kModeFlow || MODE == kModeFlowU8) && K == 2) ? CF_MINB_EVEN
+                                  : (mode_flow(MODE) && K == 2)                           ? CF_MINB_EVEN
                                                                                            : CF_MINB)
     wmc_sweeps_kernel(const SweepParams p) {
     using G = Geo<K>;
@@ -930,7 +1028,27 @@ __global__ void __launch_bounds__(kThreads,
     sw.fp = (MODE == kModeL2 || MODE == kModeL1) ? p.fdata + (int64_t)plane * p.f_plane : nullptr;
     sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
     sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
-    sw.d8p = MODE == kModeFlowU8 ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
+    sw.d8p = mode_u8_out(MODE) ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
+    sw.s8p = mode_u8_in(MODE) ? p.src8 + (int64_t)plane * p.src8_plane : nullptr;
+    if constexpr (mode_u8_in(MODE)) {
+        // column x of chunk h comes from byte (xc & 3) of staged word 0 or
+        // 1, xc = x clamped to the row (w = 0 mod 4: xc's word is always
+        // one of the two clamped words prefetch() staged)
+        const int nw = p.w >> 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int wa = min(max(sw.xf[h] >> 2, 0), nw - 1);
+            sw.o8[h][0] = 4 * wa;
+            sw.o8[h][1] = 4 * min(max((sw.xf[h] >> 2) + 1, 0), nw - 1);
+            uint32_t sel = 0;
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                const int xc = min(max(sw.xf[h] + j, 0), p.w - 1);
+                sel |= (uint32_t)(((xc >> 2) == wa ? 0 : 4) + (xc & 3)) << (4 * j);
+            }
+            sw.sel8[h] = sel;
+        }
+    }
     sw.st16 = ((reinterpret_cast<uintptr_t>(sw.d8p) | (uintptr_t)p.dst8_pitch) & 1) == 0;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K, MODE>();

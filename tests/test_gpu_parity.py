@@ -977,6 +977,50 @@ def test_widen_u8_all_bytes_every_path(P, h, w, in_pitch, out_pitch, src_off):
     assert np.all(got[:, :, w:] == -1.0)       # pitch padding untouched
 
 
+@pytest.mark.parametrize("P,h,w,pitch,iters,out8", [
+    (1, 9, 4, 4, 1, False),          # one word per row, K = 1 launch
+    (2, 17, 8, 8, 2, True),          # u8 -> u8 in one launch (kModeFlowU8InOut)
+    (3, 33, 60, 64, 3, False),       # pitched rows, one chunk; K = 2 + K = 1
+    (2, 40, 124, 124, 5, True),      # chunk boundaries at 60 / 120 columns
+    (1, 70, 256, 260, 2, False),     # several chunk pairs, pitched
+    (4, 31, 1920, 1920, 4, True),    # cfg5 row width
+    (2, 300, 512, 512, 7, False),    # long strips, odd schedule
+])
+def test_fused_u8_ingest(P, h, w, pitch, iters, out8):
+    """First launch reads u8 rows itself (kModeFlowU8In/InOut: 4-byte aligned
+    rows, w = 0 mod 4) -- every byte value, borders clamped, bit-exact vs
+    the oracle's widen-then-filter."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    rng = np.random.default_rng(P * 7919 + w + iters)
+    q = rng.integers(0, 256, size=(P, h, w), dtype=np.uint8)
+    q.reshape(-1)[:256] = np.arange(256, dtype=np.uint8)[:min(256, q.size)]
+    src = np.zeros((P, h, pitch), dtype=np.uint8)
+    src[:, :, :w] = q
+    qd = torch.from_numpy(src).cuda()
+    ref_f, bad = oracle.flow_f32(oracle.u8_to_f32(q), iters, 1.0)
+    stream = torch.cuda.current_stream().cuda_stream
+    if out8:
+        nb = int(L.cf_wmc_filter_u8_u8_workspace_bytes(w, h, P))
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        out = torch.full((P, h, w), 7, dtype=torch.uint8, device="cuda")
+        rc = L.cf_wmc_filter_u8_u8(qd.data_ptr(), pitch, h * pitch, out.data_ptr(), w, h * w,
+                                   w, h, P, iters, 1.0, ws.data_ptr(), nb, None, stream)
+        assert rc == 0
+        assert np.array_equal(out.cpu().numpy(), oracle.quantize_u8(ref_f))
+    else:
+        nb = int(L.cf_wmc_filter_workspace_bytes(w, h, w + 3, P, h * (w + 3)))
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        out = torch.full((P, h, w + 3), -1.0, device="cuda")
+        rc = L.cf_wmc_filter_u8_f32(qd.data_ptr(), pitch, h * pitch, out.data_ptr(), w, h,
+                                    w + 3, P, h * (w + 3), iters, 1.0, ws.data_ptr(), nb, None,
+                                    stream)
+        assert rc == 0
+        got = out.cpu().numpy()
+        assert_bitexact(got[:, :, :w], ref_f, "fused u8 ingest")
+        assert np.all(got[:, :, w:] == -1.0)
+
+
 @pytest.mark.parametrize("out_pitch,out_off", [(640, 0), (641, 0), (640, 1), (643, 3)])
 def test_u8_out_store_alignment(out_pitch, out_off):
     """Fused u8 quantisation (kModeFlowU8): 16-bit byte-pair stores when the
