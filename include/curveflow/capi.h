@@ -99,9 +99,10 @@ CF_API int cf_wmc_filter_query_nonfinite(const void* workspace, int32_t* first_b
 
 /* 8-bit batch variant (BASELINE cfg 5): in is u8, widened on device to    */
 /* the IEEE quotient fl(q / 255) (computed division-free as an */
-/* FMA-corrected reciprocal product, bit-identical for all 256 bytes) by a  */
-/* widening pass before the first sweep launch; out receives U^iters in    */
-/* fp32.  in_pitch / in_plane_stride in BYTES.                             */
+/* FMA-corrected reciprocal product, bit-identical for all 256 bytes):     */
+/* inside the first sweep launch when cf_wmc_filter_u8_fused() says so     */
+/* (4-byte aligned rows, w % 4 == 0), else by a widening pass before it;   */
+/* out receives U^iters in fp32.  in_pitch / in_plane_stride in BYTES.     */
 /* iters == 0 writes the widened image.                                    */
 CF_API int cf_wmc_filter_u8_f32(const uint8_t* in, int64_t in_pitch, int64_t in_plane_stride,
                                 float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,

@@ -349,6 +349,26 @@ __device__ __forceinline__ f2 select_pair(const PairD& P) {
 #ifdef CF_EXP_NOSELECT  // diagnostic builds only (wrong results): cost of the selection
     return P.d[0];
 #endif
+#ifdef CF_EXP_USSELECT  // diagnostic (wrong at exact +-ties / NaN): the map's U/S minimum
+    {
+        uint32_t U[2], Sx[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            uint32_t v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = __float_as_uint(hh ? hi(P.d[i]) : lo(P.d[i]));
+            const uint32_t a = min(min(v[0], v[1]), v[2]), b = min(min(v[3], v[4]), v[5]);
+            U[hh] = min(min(a, b), min(v[6], v[7]));
+            const int32_t sa = min(min((int32_t)v[0], (int32_t)v[1]), (int32_t)v[2]);
+            const int32_t sb = min(min((int32_t)v[3], (int32_t)v[4]), (int32_t)v[5]);
+            Sx[hh] = (uint32_t)min(min(sa, sb), min((int32_t)v[6], (int32_t)v[7]));
+        }
+        const f2 x = add2(pk(__uint_as_float(U[0]), __uint_as_float(U[1])),
+                          pk(__uint_as_float(Sx[0]), __uint_as_float(Sx[1])));
+        return pk(lo(x) > 0.0f ? __uint_as_float(Sx[0]) : __uint_as_float(U[0]),
+                  hi(x) > 0.0f ? __uint_as_float(Sx[1]) : __uint_as_float(U[1]));
+    }
+#endif
     return pk(select8(lo(P.d[0]), lo(P.d[1]), lo(P.d[2]), lo(P.d[3]), lo(P.d[4]), lo(P.d[5]),
                       lo(P.d[6]), lo(P.d[7])),
               select8(hi(P.d[0]), hi(P.d[1]), hi(P.d[2]), hi(P.d[3]), hi(P.d[4]), hi(P.d[5]),
