@@ -1021,6 +1021,47 @@ def test_fused_u8_ingest(P, h, w, pitch, iters, out8):
         assert np.all(got[:, :, w:] == -1.0)
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_u8_ingest_fuzz(seed):
+    """Random shapes, pitches, offsets and iteration counts through both u8
+    entry points: cf_wmc_filter_u8_fused() names the path (fused first
+    launch or separate widening pass) and either one equals the oracle."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    rng = np.random.default_rng(4242 + seed)
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(4):
+        P = int(rng.integers(1, 4))
+        h = int(rng.integers(1, 90))
+        w = int(rng.integers(1, 80)) * 4 - int(rng.integers(0, 2)) * int(rng.integers(1, 4))
+        pitch = w + int(rng.choice([0, 0, 4, 1, 12]))
+        off = int(rng.choice([0, 0, 4, 2]))
+        iters = int(rng.integers(1, 8))
+        q = rng.integers(0, 256, size=(P, h, w), dtype=np.uint8)
+        src = np.zeros((P, h, pitch), dtype=np.uint8)
+        src[:, :, :w] = q
+        flat = torch.zeros(src.size + 16, dtype=torch.uint8, device="cuda")
+        flat[off:off + src.size] = torch.from_numpy(src.reshape(-1)).cuda()
+        ptr = flat.data_ptr() + off
+        fused = int(L.cf_wmc_filter_u8_fused(ptr, pitch, h * pitch, w, iters))
+        assert fused == int(w % 4 == 0 and pitch % 4 == 0 and off % 4 == 0 and
+                            (h * pitch) % 4 == 0)
+        ref_f, bad = oracle.flow_f32(oracle.u8_to_f32(q), iters, 1.0)
+        tag = f"P={P} h={h} w={w} pitch={pitch} off={off} iters={iters} fused={fused}"
+        nb = int(L.cf_wmc_filter_u8_u8_workspace_bytes(w, h, P))
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        out8 = torch.full((P, h, w), 7, dtype=torch.uint8, device="cuda")
+        assert L.cf_wmc_filter_u8_u8(ptr, pitch, h * pitch, out8.data_ptr(), w, h * w, w, h, P,
+                                     iters, 1.0, ws.data_ptr(), nb, None, stream) == 0
+        assert np.array_equal(out8.cpu().numpy(), oracle.quantize_u8(ref_f)), tag
+        nbf = int(L.cf_wmc_filter_workspace_bytes(w, h, w, P, h * w))
+        wsf = torch.empty(nbf, dtype=torch.uint8, device="cuda")
+        outf = torch.empty((P, h, w), device="cuda")
+        assert L.cf_wmc_filter_u8_f32(ptr, pitch, h * pitch, outf.data_ptr(), w, h, w, P, h * w,
+                                      iters, 1.0, wsf.data_ptr(), nbf, None, stream) == 0
+        assert_bitexact(outf.cpu().numpy(), ref_f, tag)
+
+
 @pytest.mark.parametrize("out_pitch,out_off", [(640, 0), (641, 0), (640, 1), (643, 3)])
 def test_u8_out_store_alignment(out_pitch, out_off):
     """Fused u8 quantisation (kModeFlowU8): 16-bit byte-pair stores when the
