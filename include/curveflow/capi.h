@@ -256,7 +256,12 @@ CF_API int cf_wmc_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_p
                                void* workspace, size_t workspace_bytes, int32_t* first_bad_iter,
                                void* stream);
 /* mc_flow on an interleaved 8-bit image, per channel, result re-quantised. */
+/* With 4-byte aligned rows and w % 4 == 0 (cf_wmc_filter_image8_fused()   */
+/* == 1) the first sweep launch reads the interleaved bytes and the last    */
+/* writes them; otherwise separate deinterleave / interleave passes run.   */
 CF_API size_t cf_wmc_filter_image8_workspace_bytes(int32_t w, int32_t h, int32_t channels);
+CF_API int32_t cf_wmc_filter_image8_fused(const uint8_t* in, int64_t in_pitch, int32_t w,
+                                          int32_t channels, int32_t iters);
 CF_API int cf_wmc_filter_image8(const uint8_t* in, int64_t in_pitch, uint8_t* out,
                                 int64_t out_pitch, int32_t w, int32_t h, int32_t channels,
                                 int32_t iters, float dt, void* workspace, size_t workspace_bytes,

@@ -75,6 +75,7 @@ SIGNATURES = {
     "cf_wmc_filter_u8_u8": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _i32,
                                       _f32, _vp, _sz, _pi32, _vp]),
     "cf_wmc_filter_image8_workspace_bytes": (_sz, [_i32, _i32, _i32]),
+    "cf_wmc_filter_image8_fused": (_i32, [_vp, _i64, _i32, _i32, _i32]),
     "cf_wmc_filter_image8": (C.c_int, [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _f32, _vp,
                                        _sz, _pi32, _vp]),
     "cf_wmc_reduce_workspace_bytes": (_sz, [_i32, _i32, _i32]),

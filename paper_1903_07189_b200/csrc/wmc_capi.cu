@@ -370,6 +370,7 @@ struct FlowKey {
     int32_t iters; uint32_t dt; void* ws;
     const float* f; uint32_t lambda; float* d; float* d_ws; uint32_t alpha;
     uint8_t* o8; int64_t o8_pitch, o8_plane;
+    int32_t src_px, o8_px;
     // field-by-field bytes (no padding): the cache's key
     std::string bytes() const {
         std::string k;
@@ -377,6 +378,7 @@ struct FlowKey {
         put('F'); put(src0); put(src_u8); put(src_pitch); put(src_plane); put(out); put(w);
         put(h); put(pitch); put(planes); put(plane_stride); put(iters); put(dt); put(ws); put(f);
         put(lambda); put(d); put(d_ws); put(alpha); put(o8); put(o8_pitch); put(o8_plane);
+        put(src_px); put(o8_px);
         return k;
     }
 };
@@ -547,10 +549,11 @@ CF_API int32_t cf_wmc_filter_launches(int32_t w, int32_t h, int32_t planes, int3
     return (int32_t)schedule(iters, flow_levels(w, h, planes)).size();
 }
 
-static bool u8_fusable(const void* src0, int64_t pitch, int64_t plane, int32_t w);
+static bool u8_fusable(const void* src0, int64_t pitch, int64_t plane, int32_t w, int32_t px,
+                       int32_t planes);
 CF_API int32_t cf_wmc_filter_u8_fused(const void* in, int64_t in_pitch, int64_t in_plane_stride,
                                       int32_t w, int32_t iters) {
-    return iters > 0 && in && w > 0 && u8_fusable(in, in_pitch, in_plane_stride, w) ? 1 : 0;
+    return iters > 0 && in && w > 0 && u8_fusable(in, in_pitch, in_plane_stride, w, 1, 1) ? 1 : 0;
 }
 
 CF_API void cf_kernel_bank_x12(int32_t* out72) {
@@ -602,27 +605,35 @@ struct DataTerm {            // solve_l2_area / solve_l1_area (f != nullptr)
 };
 
 // The first launch can read u8 rows itself (cfk::kModeFlowU8In) when every
-// row starts on a 4-byte boundary and holds whole 4-byte words.
+// row starts on a 4-byte boundary and w % 4 == 0, so the words holding a
+// row's pixels never reach past its last pixel's word: planar rows (pixel
+// stride px = 1, plane stride a multiple of 4) or interleaved channels
+// (plane stride 1, px = planes <= 3; two staged words per lane need C = 2).
 // CF_U8_FUSE=0 forces the separate widening pass (A/B measurements).
-static bool u8_fusable(const void* src0, int64_t pitch, int64_t plane, int32_t w) {
+static bool u8_fusable(const void* src0, int64_t pitch, int64_t plane, int32_t w, int32_t px,
+                       int32_t planes) {
     static const bool enabled = [] {
         const char* e = std::getenv("CF_U8_FUSE");
         return !(e && e[0] == '0');
     }();
-    return enabled && w % 4 == 0 &&
-           ((reinterpret_cast<uintptr_t>(src0) | (uintptr_t)pitch | (uintptr_t)plane) & 3) == 0;
+    if (!enabled || w % 4 != 0 || ((reinterpret_cast<uintptr_t>(src0) | (uintptr_t)pitch) & 3))
+        return false;
+    if (px == 1) return (plane & 3) == 0;
+    return cfk::C == 2 && px <= 3 && plane == 1 && planes == px;
 }
 
 struct Out8 {               // fused save-time quantisation of the last launch
     uint8_t* p = nullptr;
     int64_t pitch = 0, plane = 0;
+    int32_t px = 1;         // bytes between a row's pixels (channels when interleaved)
 };
 
 // Enqueue one filter / solver run: the launches of schedule(iters) on `s`.
 static int enqueue_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t src_plane,
                         float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
                         int64_t plane_stride, int32_t iters, float dt, void* workspace,
-                        cudaStream_t s, const DataTerm& dterm, const Out8& out8) {
+                        cudaStream_t s, const DataTerm& dterm, const Out8& out8,
+                        int32_t src_px) {
     DevInfo d;
     if (int rc = device_info(&d)) return rc;
     int32_t* flag = reinterpret_cast<int32_t*>(workspace);
@@ -638,8 +649,9 @@ static int enqueue_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_
     float* dnxt = dterm.d_ws;
     // u8 input: widened inside the first launch's row loads
     // when the bytes allow 4-byte copies, else by a separate pass
-    const bool fuse8 =
-        src_u8 && !ks.empty() && u8_fusable(src0, src_pitch, src_plane, w) && !dterm.f;
+    const bool fuse8 = src_u8 && !ks.empty() &&
+                       u8_fusable(src0, src_pitch, src_plane, w, src_px, planes) && !dterm.f;
+    if (src_u8 && src_px != 1 && !fuse8) return CF_EINVAL;  // interleaved: fused only
     if (src_u8) {
         // the widened image (or the first launch's output) goes to whichever
         // buffer makes the final launch land in `out`
@@ -663,11 +675,12 @@ static int enqueue_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_
         p.alpha = dterm.alpha; p.neg_inv_alpha = -(1.0f / dterm.alpha);
         if (out8.p && i + 1 == ks.size()) {  // last launch: u8 bytes instead of fp32
             p.dst8 = out8.p; p.dst8_pitch = out8.pitch; p.dst8_plane = out8.plane;
+            p.dst8_px = out8.px;
         }
         const bool in8 = fuse8 && i == 0;    // first launch: u8 rows in
         if (in8) {
             p.src8 = static_cast<const uint8_t*>(src0);
-            p.src8_pitch = src_pitch; p.src8_plane = src_plane;
+            p.src8_pitch = src_pitch; p.src8_plane = src_plane; p.src8_px = src_px;
         }
         const int rc = dterm.d          ? launch<cfk::kModeL1>(p, ks[i], d, s)
                        : dterm.f        ? launch<cfk::kModeL2>(p, ks[i], d, s)
@@ -698,7 +711,7 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
                     float* out, int32_t w, int32_t h, int64_t pitch, int32_t planes,
                     int64_t plane_stride, int32_t iters, float dt, void* workspace,
                     int32_t* first_bad_iter, cudaStream_t s, DataTerm dterm = {},
-                    Out8 out8 = {}) {
+                    Out8 out8 = {}, int32_t src_px = 1) {
     FlowKey key{};
     CF_CUDA(cudaGetDevice(&key.dev));
     key.src0 = src0; key.src_u8 = src_u8; key.src_pitch = src_pitch; key.src_plane = src_plane;
@@ -707,13 +720,41 @@ static int run_flow(const void* src0, bool src_u8, int64_t src_pitch, int64_t sr
     key.ws = workspace; key.f = dterm.f; key.lambda = f32_bits(dterm.lambda);
     key.d = dterm.d; key.d_ws = dterm.d_ws; key.alpha = f32_bits(dterm.alpha);
     key.o8 = out8.p; key.o8_pitch = out8.pitch; key.o8_plane = out8.plane;
+    key.src_px = src_px; key.o8_px = out8.px;
     const int rc = run_cached(key.dev, key.bytes(), s, [&](cudaStream_t st) {
         return enqueue_flow(src0, src_u8, src_pitch, src_plane, out, w, h, pitch, planes,
-                            plane_stride, iters, dt, workspace, st, dterm, out8);
+                            plane_stride, iters, dt, workspace, st, dterm, out8, src_px);
     });
     if (rc) return rc;
     if (first_bad_iter) return cf_wmc_filter_query_nonfinite(workspace, first_bad_iter, s);
     return CF_OK;
+}
+
+// Interleaved 8-bit image in and out (wmc_io.cu's cf_wmc_filter_image8;
+// arguments validated there): channel c is plane c with plane stride 1 and
+// pixel stride `channels`, widened in the first launch and quantised in the
+// last, when cf_internal_image8_fusable() says the input can be read that way.
+extern "C" int cf_internal_image8_fusable(const uint8_t* in, int64_t in_pitch, int32_t w,
+                                          int32_t channels, int32_t iters) {
+    // gray: one plane (its stride unused); RGB: interleaved, plane stride 1
+    return iters > 0 && u8_fusable(in, in_pitch, channels == 1 ? 0 : 1, w, channels, channels) ? 1
+                                                                                               : 0;
+}
+CF_API int32_t cf_wmc_filter_image8_fused(const uint8_t* in, int64_t in_pitch, int32_t w,
+                                          int32_t channels, int32_t iters) {
+    return in && w > 0 && (channels == 1 || channels == 3)
+               ? cf_internal_image8_fusable(in, in_pitch, w, channels, iters)
+               : 0;
+}
+extern "C" int cf_internal_filter_image8(const uint8_t* in, int64_t in_pitch, int32_t channels,
+                                         float* fbuf, int32_t w, int32_t h, int32_t iters,
+                                         float dt, void* fws, uint8_t* out, int64_t out_pitch,
+                                         int32_t* first_bad_iter, void* stream) {
+    Out8 o8;
+    const int64_t plane = channels == 1 ? 0 : 1;
+    o8.p = out; o8.pitch = out_pitch; o8.plane = plane; o8.px = channels;
+    return run_flow(in, true, in_pitch, plane, fbuf, w, h, w, channels, (int64_t)w * h, iters, dt,
+                    fws, first_bad_iter, (cudaStream_t)stream, DataTerm{}, o8, channels);
 }
 
 // u8 frames in, u8 frames out with the quantisation fused into the last

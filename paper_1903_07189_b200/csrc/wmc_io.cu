@@ -16,6 +16,12 @@
 #include "../../include/curveflow/capi.h"
 
 extern "C" void cf_internal_set_cuda_error(int e);  // wmc_capi.cu (not exported)
+extern "C" int cf_internal_image8_fusable(const uint8_t* in, int64_t in_pitch, int32_t w,
+                                          int32_t channels, int32_t iters);
+extern "C" int cf_internal_filter_image8(const uint8_t* in, int64_t in_pitch, int32_t channels,
+                                         float* fbuf, int32_t w, int32_t h, int32_t iters,
+                                         float dt, void* fws, uint8_t* out, int64_t out_pitch,
+                                         int32_t* first_bad_iter, void* stream);
 extern "C" int cf_internal_filter_u8_u8(const uint8_t* in, int64_t in_pitch, int64_t in_plane,
                                         float* fbuf, int32_t w, int32_t h, int32_t planes,
                                         int32_t iters, float dt, void* fws, uint8_t* out,
@@ -130,6 +136,14 @@ CF_API int cf_wmc_filter_image8(const uint8_t* in, int64_t in_pitch, uint8_t* ou
     const size_t off = align256((size_t)(channels * plane) * sizeof(float));
     void* fws = reinterpret_cast<char*>(workspace) + off;
     const size_t fws_bytes = workspace_bytes - off;
+    if (cf_internal_image8_fusable(in, in_pitch, w, channels, iters)) {
+        // deinterleave + widen inside the first sweep launch, clamp + round +
+        // interleave inside the last (4-byte aligned rows, w % 4 == 0)
+        if (!(dt > 0.0f) || dt > 1.0f) return CF_EINVAL;
+        if (first_bad_iter) *first_bad_iter = 0;
+        return cf_internal_filter_image8(in, in_pitch, channels, planes, w, h, iters, dt, fws, out,
+                                         out_pitch, first_bad_iter, stream);
+    }
     int rc = cf_image8_to_planes_f32(in, in_pitch, w, h, channels, planes, w, plane, stream);
     if (rc) return rc;
     rc = cf_wmc_filter_f32(planes, w, h, w, channels, plane, iters, dt, fws, fws_bytes,

@@ -116,12 +116,17 @@ struct SweepParams {
     // instead of fp32 to dst.
     uint8_t* dst8;
     int64_t dst8_pitch, dst8_plane;
+    int32_t dst8_px;          // bytes between a row's pixels (1 planar; channels interleaved)
     // Fused load-time widening (kModeFlowU8In / kModeFlowU8InOut, the u8
     // paths' first launch): level-0 rows come from u8 bytes at src8 (global
-    // row src_row0 of plane 0) instead of src.  Host contract: src8, pitch
-    // and plane stride multiples of 4 bytes, w a multiple of 4.
+    // row src_row0 of plane 0) instead of src, pixel x of plane p at byte
+    // p * src8_plane + x * src8_px of its row.  Host contract (u8_fusable):
+    // src8 and the pitch multiples of 4 bytes, w a multiple of 4, and either
+    // planar (px 1, plane stride a multiple of 4) or interleaved (plane
+    // stride 1, px = channels <= 3, C = 2).
     const uint8_t* src8;
     int64_t src8_pitch, src8_plane;
+    int32_t src8_px;
     // MODE == kModeL2 (solve_l2_area): data term f and lambda
     const float* fdata;       // global row 0 of plane 0 (same column geometry as src)
     int64_t f_pitch, f_plane; // elements
@@ -428,9 +433,10 @@ struct SweepWarp {
     const float* dsp;             // plane base of d^t (kModeL1)
     float* ddp;                   // plane base of d^{t+K} (kModeL1)
     uint8_t* d8p;                 // plane base of the u8 output (fused quantisation)
-    const uint8_t* s8p;           // plane base of the u8 input (fused widening)
+    const uint8_t* s8p;           // u8 input: 4-byte aligned base of this plane's rows
     uint32_t sel8[2];             // byte_perm selectors: chunk h's C input bytes from its words
     int o8[2][2];                 // byte offsets in a u8 row of chunk h's staged words
+    int nw8;                      // staged words per chunk (1 or 2)
     uint32_t pend8[4];            // staged words of row t + 1, widened at the end of step t
     uint32_t sbase;               // this warp's shared memory (ring 0, then rings 1..K-1)
     uint32_t lbase;               // sbase + this lane's neighbourhood offset (8*C*lane)
@@ -483,7 +489,8 @@ struct SweepWarp {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int k = 0; k < kNW8; ++k) cp_async4(s + 4 * kNW8 * h + 4 * k, row8 + o8[h][k]);
+                for (int k = 0; k < 2; ++k)
+                    if (k < nw8) cp_async4(s + 4 * nw8 * h + 4 * k, row8 + o8[h][k]);
             return;
         }
         const float* row = srcp + (int64_t)(y - P.src_row0) * P.src_pitch;
@@ -514,17 +521,17 @@ struct SweepWarp {
     }
 
     static constexpr bool kU8In = mode_u8_in(MODE);
-    // Words per chunk and lane: a lane's C columns start at xf = chunk * S
-    // - K + C * lane, so with C = 2 and K even they sit in one aligned word.
-    static constexpr int kNW8 = (C == 2 && K % 2 == 0) ? 1 : 2;
-    // staged words (2 * kNW8 of them) inside the lane's 8*C-byte region at
-    // +8, aligned to their total size (C = 4: at +16)
+    // Staged words per chunk and lane (nw8): a lane's C columns start at
+    // xf = chunk * S - K + C * lane, so planar rows at C = 2 and even K put
+    // them in one aligned word; otherwise they span two.  The 2 * nw8 words
+    // sit inside the lane's 8*C-byte region at +8, aligned to their total
+    // size (C = 4: at +16).
     static constexpr int k8Stage = C == 4 ? 16 : 8;
 
     // kU8In: this lane's staged words of row y (landed: after the wait)
     __device__ __forceinline__ void load8(int y, uint32_t (&wd)[4]) const {
         const uint32_t a = sbase + (uint32_t)(y & (kRS - 1)) * kRowBytes + 8 * C * lane + k8Stage;
-        if constexpr (kNW8 == 1) {
+        if (C == 2 && nw8 == 1) {
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wd[0]), "=r"(wd[2]) : "r"(a));
             wd[1] = wd[0]; wd[3] = wd[2];
         } else if constexpr (C == 4) {
@@ -717,7 +724,7 @@ struct SweepWarp {
     __device__ __forceinline__ void store_row8(uint8_t* row, const f2 (&nv)[C]) const {
         if constexpr (FAST && C == 2 && (G::A & 1) == 0) {
             if (!outc[0]) return;
-            if (st16) {  // even row addresses (base and pitch)
+            if (st16) {  // planar, even row addresses (base and pitch)
                 const uint32_t b0 = quantize_u8(lo(nv[0])) | (quantize_u8(lo(nv[1])) << 8);
                 const uint32_t b1 = quantize_u8(hi(nv[0])) | (quantize_u8(hi(nv[1])) << 8);
                 *reinterpret_cast<uint16_t*>(row + xf[0]) = (uint16_t)b0;
@@ -725,11 +732,12 @@ struct SweepWarp {
                 return;
             }
         }
+        const int px = P.dst8_px;
 #pragma unroll
         for (int j = 0; j < C; ++j) {
             if (!outc[j]) continue;
-            if (out_h[0] && xf[0] + j < P.w) row[xf[0] + j] = (uint8_t)quantize_u8(lo(nv[j]));
-            if (out_h[1] && xf[1] + j < P.w) row[xf[1] + j] = (uint8_t)quantize_u8(hi(nv[j]));
+            if (out_h[0] && xf[0] + j < P.w) row[px * (xf[0] + j)] = (uint8_t)quantize_u8(lo(nv[j]));
+            if (out_h[1] && xf[1] + j < P.w) row[px * (xf[1] + j)] = (uint8_t)quantize_u8(hi(nv[j]));
         }
     }
 
@@ -1049,27 +1057,36 @@ __global__ void __launch_bounds__(kThreads,
     sw.dsp = MODE == kModeL1 ? p.dsrc + (int64_t)plane * p.f_plane : nullptr;
     sw.ddp = MODE == kModeL1 ? p.ddst + (int64_t)plane * p.f_plane : nullptr;
     sw.d8p = mode_u8_out(MODE) ? p.dst8 + (int64_t)plane * p.dst8_plane : nullptr;
-    sw.s8p = mode_u8_in(MODE) ? p.src8 + (int64_t)plane * p.src8_plane : nullptr;
+    sw.s8p = nullptr;
     if constexpr (mode_u8_in(MODE)) {
-        // column x of chunk h comes from byte (xc & 3) of staged word 0 or
-        // 1, xc = x clamped to the row (w = 0 mod 4: xc's word is always
-        // one of the two clamped words prefetch() staged)
-        const int nw = p.w >> 2;
+        // Pixel x of this plane is byte c8 + px * x of the aligned row base
+        // (c8: the plane offset's low two bits -- an interleaved channel).
+        // Column x of chunk h comes from byte b & 3 of staged word 0 or 1,
+        // b = c8 + px * xc, xc = x clamped to the row: the words of a lane's
+        // clamped columns are always the two clamped words prefetch() stages
+        // (w = 0 mod 4; px <= 3 at C = 2).
+        const uintptr_t a8 = reinterpret_cast<uintptr_t>(p.src8 + (int64_t)plane * p.src8_plane);
+        const int c8 = (int)(a8 & 3u), px = p.src8_px;
+        sw.s8p = reinterpret_cast<const uint8_t*>(a8 - (uintptr_t)c8);
+        const int nw = ((c8 + px * (p.w - 1)) >> 2) + 1;  // words holding the row's pixels
+        sw.nw8 = (C == 2 && K % 2 == 0 && px == 1 && c8 == 0) ? 1 : 2;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int wa = min(max(sw.xf[h] >> 2, 0), nw - 1);
+            const int w0 = (c8 + px * sw.xf[h]) >> 2;  // floor (xf may be negative)
+            const int wa = min(max(w0, 0), nw - 1);
             sw.o8[h][0] = 4 * wa;
-            sw.o8[h][1] = 4 * min(max((sw.xf[h] >> 2) + 1, 0), nw - 1);
+            sw.o8[h][1] = 4 * min(max(w0 + 1, 0), nw - 1);
             uint32_t sel = 0;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
-                const int xc = min(max(sw.xf[h] + j, 0), p.w - 1);
-                sel |= (uint32_t)(((xc >> 2) == wa ? 0 : 4) + (xc & 3)) << (4 * j);
+                const int b = c8 + px * min(max(sw.xf[h] + j, 0), p.w - 1);
+                sel |= (uint32_t)(((b >> 2) == wa ? 0 : 4) + (b & 3)) << (4 * j);
             }
             sw.sel8[h] = sel;
         }
     }
-    sw.st16 = ((reinterpret_cast<uintptr_t>(sw.d8p) | (uintptr_t)p.dst8_pitch) & 1) == 0;
+    sw.st16 = p.dst8_px == 1 &&
+              ((reinterpret_cast<uintptr_t>(sw.d8p) | (uintptr_t)p.dst8_pitch) & 1) == 0;
     sw.sbase = (uint32_t)__cvta_generic_to_shared(smem) +
                (uint32_t)(threadIdx.x >> 5) * smem_bytes_per_warp<K, MODE>();
     sw.lbase = sw.sbase + 8 * C * sw.lane;

@@ -220,6 +220,48 @@ def test_flow_image8_interleaved(ch):
         cf.mc_flow_image8(np.zeros((4, 4, 2), np.uint8), cf.FlowConfig(iters=1))
 
 
+@pytest.mark.parametrize("ch,h,w,pitch,off,iters", [
+    (3, 17, 8, 24, 0, 1),        # fused, one K = 1 launch reading and writing RGB
+    (3, 33, 64, 192, 0, 2),      # fused u8 -> u8 in one K = 2 launch
+    (3, 40, 124, 376, 0, 5),     # chunk boundaries, pitched rows, odd schedule
+    (3, 70, 256, 768, 4, 6),     # several chunk pairs, 4-byte offset
+    (1, 45, 132, 132, 0, 3),     # gray: planar fused path
+    (3, 30, 66, 198, 0, 4),      # w % 4 != 0: separate passes
+    (3, 30, 64, 194, 0, 4),      # unaligned pitch: separate passes
+    (3, 21, 64, 192, 1, 3),      # unaligned base: separate passes
+])
+def test_image8_fused_interleaved(ch, h, w, pitch, off, iters):
+    """Interleaved RGB / gray bytes read by the first sweep launch and written
+    by the last (plane stride 1, pixel stride = channels), or the separate
+    deinterleave / interleave passes -- every path equals the oracle."""
+    from paper_1903_07189_b200._lib import lib
+    L = lib()
+    rng = np.random.default_rng(ch * 1000 + w + iters)
+    img = rng.integers(0, 256, size=(h, w, ch), dtype=np.uint8)
+    img.reshape(-1)[:256] = np.arange(256, dtype=np.uint8)[:min(256, img.size)]
+    src = np.zeros((h, pitch), dtype=np.uint8)
+    src[:, :w * ch] = img.reshape(h, w * ch)
+    flat = torch.zeros(src.size + 16, dtype=torch.uint8, device="cuda")
+    flat[off:off + src.size] = torch.from_numpy(src.reshape(-1)).cuda()
+    ptr = flat.data_ptr() + off
+    fused = int(L.cf_wmc_filter_image8_fused(ptr, pitch, w, ch, iters))
+    assert fused == int(w % 4 == 0 and pitch % 4 == 0 and off % 4 == 0)
+    out_pitch = w * ch + 5
+    out = torch.full((h, out_pitch), 9, dtype=torch.uint8, device="cuda")
+    nb = int(L.cf_wmc_filter_image8_workspace_bytes(w, h, ch))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bad = C.c_int32(-1)
+    rc = L.cf_wmc_filter_image8(ptr, pitch, out.data_ptr(), out_pitch, w, h, ch, iters, 1.0,
+                                ws.data_ptr(), nb, C.byref(bad),
+                                torch.cuda.current_stream().cuda_stream)
+    assert rc == 0 and bad.value == 0
+    got = out.cpu().numpy()
+    ref, _ = oracle.flow_image8(img if ch == 3 else img[:, :, 0], iters, 1.0)
+    assert np.array_equal(got[:, :w * ch].reshape(img.shape), ref.reshape(img.shape)), \
+        f"fused={fused}"
+    assert np.all(got[:, w * ch:] == 9)             # pitch padding untouched
+
+
 @pytest.mark.parametrize("lam,dt,iters", [(0.0, 0.15, 9), (3.0, 0.15, 1), (3.0, 0.15, 20),
                                           (20.0, 0.05, 37), (150.0, 0.002, 10)])
 def test_solve_l2_area_bitexact(lam, dt, iters):
