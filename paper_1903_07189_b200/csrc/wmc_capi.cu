@@ -126,7 +126,13 @@ void plan_strips(cfk::SweepParams& p, int K, int slots) {
 #define CF_PLAN_OVH 3.0  // measured: 1-4 rows +0.6 % on cfg4 over 6, cfg3 unchanged, 1 row -11 % on cfg3
 #endif
     const double overhead = (K - 1) + CF_PLAN_OVH;  // warm-up rows + fixed per-task cost (rows)
-    const int max_strips = std::max(1, rows / std::max(8, 4 * K));
+#ifndef CF_MIN_STRIP
+#define CF_MIN_STRIP 8   // output rows per strip at least max(CF_MIN_STRIP, CF_MIN_STRIP_K * K)
+#endif
+#ifndef CF_MIN_STRIP_K
+#define CF_MIN_STRIP_K 4
+#endif
+    const int max_strips = std::max(1, rows / std::max(CF_MIN_STRIP, CF_MIN_STRIP_K * K));
     double best_cost = 1e300;
     int best = 1;
     for (int ns = 1; ns <= max_strips; ++ns) {
