@@ -227,6 +227,10 @@ __device__ __forceinline__ double lane_tree8(const double (&t)[8]) {
     return __dadd_rn(__dadd_rn(__dadd_rn(t[0], t[1]), __dadd_rn(t[2], t[3])),
                      __dadd_rn(__dadd_rn(t[4], t[5]), __dadd_rn(t[6], t[7])));
 }
+// (CF_MAP_COLS=2 experiment builds only: not the energy's pinned order)
+__device__ __forceinline__ double lane_tree8(const double (&t)[4]) {
+    return __dadd_rn(__dadd_rn(t[0], t[1]), __dadd_rn(t[2], t[3]));
+}
 
 // One warp's strip.  Ring slot of row r: (r - (ys - 1)) & 7.
 // INTERIOR: every column x0-1 .. x0+256 inside the image (no clamping).
