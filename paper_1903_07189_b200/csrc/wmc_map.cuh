@@ -233,13 +233,15 @@ __device__ __forceinline__ double lane_tree8(const double (&t)[4]) {
 }
 
 // One warp's strip.  Ring slot of row r: (r - (ys - 1)) & 7.
-// INTERIOR: every column x0-1 .. x0+256 inside the image (no clamping).
-template <bool INTERIOR, int QK>  // QK > 0: the fused energy epilogue of that power
+// INTERIOR: every column x0-1 .. x0+256 inside the image (no clamping);
+// ST128: INTERIOR with 16-byte aligned output rows (vector stores).
+template <bool INTERIOR, int QK, bool ST128 = false>  // QK > 0: the fused energy epilogue
 struct MapWarp {
     static constexpr bool ENERGY = QK > 0;
     const MapParams& p;
     int lane, ys, ye, x0;
     const float* src;      // plane base
+    int64_t pf_step;       // src row pitch in bytes
     const char* pf;        // column x0 of the next row to prefetch (row clamp(yp))
     int yp;
     uint32_t sbase;
@@ -280,14 +282,14 @@ struct MapWarp {
                           row + min(max(x0 + c0 + 16 * kMapCopies, 0), p.w - 1));
         }
         // clamp-to-edge rows: rows < 0 read row 0, rows >= h read row h-1
-        if (yp >= 0 && yp < p.h - 1) pf += p.src_pitch * 4;
+        if ((unsigned)yp < (unsigned)(p.h - 1)) pf += pf_step;
         ++yp;
     }
 
     // 16-byte stores (chunk 0 = lo halves at x0 + 4i .., chunk 1 = hi halves
     // at x0 + 128 + 4i ..) where the rows are 16-byte aligned
     __device__ __forceinline__ void store(float* row, const f2 (&nv)[kMapCols]) const {
-        if (INTERIOR && p.st128) {
+        if (ST128) {
             if constexpr (kMapCols == 4) {
                 asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row),
                              "f"(lo(nv[0])), "f"(lo(nv[1])), "f"(lo(nv[2])), "f"(lo(nv[3]))
@@ -332,6 +334,7 @@ struct MapWarp {
             }
         }
         float* sp = dst ? dst + (int64_t)ys * p.dst_pitch + x0 + kMapCols * lane : nullptr;
+        const int64_t dpitch = p.dst_pitch;
         for (int y = ys; y < ye; ++y) {
             const int k = y - ys;  // slot of row y-1
             // rows y-1 .. y+1 landed: of the PD + k groups issued (rows up to
@@ -402,7 +405,7 @@ struct MapWarp {
             }
             if (!ENERGY || p.dst) {
                 store(sp, out);
-                sp += p.dst_pitch;
+                sp += dpitch;
             }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");  // no copy outlives the warp
@@ -443,6 +446,7 @@ __global__ void __launch_bounds__(32 * kMapWarps, QK ? CF_MAP_MINB_ENERGY : CF_M
         mw.ye = min(ys + p.strip_rows, p.h);
         mw.x0 = x0;
         mw.src = src;
+        mw.pf_step = p.src_pitch * 4;
         mw.yp = ys - 1;
         mw.sbase = sbase;
         // window columns C*i-1 .. C*i+C: 16-byte chunks C*i/2 + k (swizzled)
@@ -454,7 +458,12 @@ __global__ void __launch_bounds__(32 * kMapWarps, QK ? CF_MAP_MINB_ENERGY : CF_M
         mw.cpe = 16u * map_swz_chunk((uint32_t)(lane >> 2)) + 4u * (lane & 3);
         mw.cpo = 16u * (map_swz_chunk((uint32_t)(8 + (lane >> 2))) - 8u) + 4u * (lane & 3);
     };
-    if (x0 > 0 && x0 + 2 * kMapChunk < p.w) {
+    if (x0 > 0 && x0 + 2 * kMapChunk < p.w && p.st128) {
+        MapWarp<true, QK, true> mw(p);
+        init(mw);
+        mw.pf = reinterpret_cast<const char*>(row0 + x0);
+        mw.run(dst);
+    } else if (x0 > 0 && x0 + 2 * kMapChunk < p.w) {
         MapWarp<true, QK> mw(p);
         init(mw);
         mw.pf = reinterpret_cast<const char*>(row0 + x0);
