@@ -56,7 +56,7 @@ __device__ __forceinline__ int32_t smin8(const uint32_t (&v)[8]) {
 // x is 0 (|b| is the tied magnitude either way) or NaN (no tie either way).
 // The fast path returns b and a "rare" flag per pixel (tie, or tournament
 // needed); map_pair_fix redoes flagged pixels.
-__device__ __forceinline__ f2 map_fast(const PairD& D, bool& rare) {
+__device__ __forceinline__ void map_fast_s(const PairD& D, float& b0, float& b1, bool& rare) {
     uint32_t dl[8], dh[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -68,8 +68,8 @@ __device__ __forceinline__ f2 map_fast(const PairD& D, bool& rare) {
     const f2 x = add2(pk(__uint_as_float(U0), __uint_as_float(U1)),
                       pk(__int_as_float(S0), __int_as_float(S1)));
     const float x0 = lo(x), x1 = hi(x);
-    const float b0 = x0 > 0.0f ? __int_as_float(S0) : __uint_as_float(U0);
-    const float b1 = x1 > 0.0f ? __int_as_float(S1) : __uint_as_float(U1);
+    b0 = x0 > 0.0f ? __int_as_float(S0) : __uint_as_float(U0);
+    b1 = x1 > 0.0f ? __int_as_float(S1) : __uint_as_float(U1);
     const float tau0 = __fmaf_rn(fabsf(lo(D.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b0), 0x1.0p-20f));
     const float tau1 = __fmaf_rn(fabsf(hi(D.n12u)), 0x1.8p-19f, __fmul_rn(fabsf(b1), 0x1.0p-20f));
     // A superset of {near tie} u {tournament needed}, two predicates a pixel:
@@ -78,6 +78,10 @@ __device__ __forceinline__ f2 map_fast(const PairD& D, bool& rare) {
     // unordered compare.  map_pair_fix applies the exact rule.
     rare = ((U0 != (uint32_t)S0) & !(fabsf(x0) > tau0)) |
            ((U1 != (uint32_t)S1) & !(fabsf(x1) > tau1));
+}
+__device__ __forceinline__ f2 map_fast(const PairD& D, bool& rare) {
+    float b0, b1;
+    map_fast_s(D, b0, b1, rare);
     return pk(b0, b1);
 }
 
@@ -138,6 +142,22 @@ __device__ __forceinline__ f2 map_pair(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e,
     Tm = t0;
     const f2 best = map_fast(D, rare);
     return mul2(best, kC12x2);
+}
+// The same with the pair's two results as scalars (h0: chunk 0, h1: chunk
+// 1): the streaming kernel's 16-byte stores take four chunk-0 values in
+// consecutive registers, which a packed pair would have to be unpacked into.
+__device__ __forceinline__ void map_pair_s(f2 a, f2 b, f2 c, f2 l, f2 u, f2 r, f2 e, f2 f, f2 g,
+                                           f2 Wm, f2 W0, f2& Hc, f2& Tm, float& h0, float& h1,
+                                           bool& rare) {
+    PairD D;
+    f2 hb, t0;
+    pair_d(a, b, c, l, u, r, e, f, g, Wm, W0, Hc, Tm, hb, t0, D);
+    Hc = hb;
+    Tm = t0;
+    float b0, b1;
+    map_fast_s(D, b0, b1, rare);
+    h0 = __fmul_rn(b0, 0x1.555556p-4f);  // fl(1/12): the lanes of mul2(best, kC12x2)
+    h1 = __fmul_rn(b1, 0x1.555556p-4f);
 }
 
 // ---- the streaming map kernel ---------------------------------------------
@@ -242,6 +262,7 @@ struct MapWarp {
     int lane, ys, ye, x0;
     const float* src;      // plane base
     int64_t pf_step;       // src row pitch in bytes
+    bool tail4;            // lanes 0-3 also copy the row's last 4 words
     const char* pf;        // column x0 of the next row to prefetch (row clamp(yp))
     int yp;
     uint32_t sbase;
@@ -270,14 +291,14 @@ struct MapWarp {
 #pragma unroll
             for (int kk = 0; kk < kMapCopies; ++kk)
                 cp_async4(s + 128 * kk + ((kk & 1) ? cpo : cpe), g + 64 * kk);
-            if (lane < 4) cp_async4(s + 128 * kMapCopies + cpe, g + 64 * kMapCopies);
+            if (tail4) cp_async4(s + 128 * kMapCopies + cpe, g + 64 * kMapCopies);
         } else {  // image-edge warp: clamped columns
             const float* row = reinterpret_cast<const float*>(pf);
 #pragma unroll
             for (int kk = 0; kk < kMapCopies; ++kk)
                 cp_async4(s + 128 * kk + ((kk & 1) ? cpo : cpe),
                           row + min(max(x0 + c0 + 16 * kk, 0), p.w - 1));
-            if (lane < 4)
+            if (tail4)
                 cp_async4(s + 128 * kMapCopies + cpe,
                           row + min(max(x0 + c0 + 16 * kMapCopies, 0), p.w - 1));
         }
@@ -288,28 +309,27 @@ struct MapWarp {
 
     // 16-byte stores (chunk 0 = lo halves at x0 + 4i .., chunk 1 = hi halves
     // at x0 + 128 + 4i ..) where the rows are 16-byte aligned
-    __device__ __forceinline__ void store(float* row, const f2 (&nv)[kMapCols]) const {
+    __device__ __forceinline__ void store(float* row, const float (&ol)[kMapCols],
+                                          const float (&oh)[kMapCols]) const {
         if (ST128) {
             if constexpr (kMapCols == 4) {
-                asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row),
-                             "f"(lo(nv[0])), "f"(lo(nv[1])), "f"(lo(nv[2])), "f"(lo(nv[3]))
-                             : "memory");
+                asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row), "f"(ol[0]),
+                             "f"(ol[1]), "f"(ol[2]), "f"(ol[3]) : "memory");
                 asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + kMapChunk),
-                             "f"(hi(nv[0])), "f"(hi(nv[1])), "f"(hi(nv[2])), "f"(hi(nv[3]))
-                             : "memory");
+                             "f"(oh[0]), "f"(oh[1]), "f"(oh[2]), "f"(oh[3]) : "memory");
             } else {
-                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(row), "f"(lo(nv[0])),
-                             "f"(lo(nv[1])) : "memory");
-                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(row + kMapChunk),
-                             "f"(hi(nv[0])), "f"(hi(nv[1])) : "memory");
+                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(row), "f"(ol[0]), "f"(ol[1])
+                             : "memory");
+                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(row + kMapChunk), "f"(oh[0]),
+                             "f"(oh[1]) : "memory");
             }
             return;
         }
 #pragma unroll
         for (int j = 0; j < kMapCols; ++j) {
             const int xa = x0 + kMapCols * lane + j;
-            if (INTERIOR || xa < p.w) row[j] = lo(nv[j]);
-            if (INTERIOR || xa + kMapChunk < p.w) row[kMapChunk + j] = hi(nv[j]);
+            if (INTERIOR || xa < p.w) row[j] = ol[j];
+            if (INTERIOR || xa + kMapChunk < p.w) row[kMapChunk + j] = oh[j];
         }
     }
 
@@ -347,7 +367,8 @@ struct MapWarp {
             lds_row6(slot(k), co, m);
             lds_row6(slot(k + 1), co, o);
             lds_row6(slot(k + 2), co, q);
-            f2 V[kMapNb], W[kMapNb - 1], out[kMapCols];
+            f2 V[kMapNb], W[kMapNb - 1];
+            float ol[kMapCols], oh[kMapCols];  // chunk 0 / chunk 1 results
 #pragma unroll
             for (int i = 0; i < kMapNb; ++i) V[i] = add2(m[i], q[i]);
 #pragma unroll
@@ -357,7 +378,11 @@ struct MapWarp {
             for (int j = 0; j < kMapCols; ++j) {
                 bool r;
 #if defined(CF_MAP_EXP) && CF_MAP_EXP == 1  // diagnostic (wrong results): data movement only
-                out[j] = add2(add2(m[j + 1], q[j + 1]), W[j]);
+                {
+                    const f2 v = add2(add2(m[j + 1], q[j + 1]), W[j]);
+                    ol[j] = lo(v);
+                    oh[j] = hi(v);
+                }
                 r = false;
 #elif defined(CF_MAP_EXP) && CF_MAP_EXP == 2  // diagnostic (wrong results): no selection
                 {
@@ -367,22 +392,28 @@ struct MapWarp {
                            q[j + 2], W[j], W[j + 1], hc[j], tm[j], hb, t0, D);
                     hc[j] = hb;
                     tm[j] = t0;
-                    out[j] = add2(add2(add2(D.d[0], D.d[1]), add2(D.d[2], D.d[3])),
-                                  add2(add2(D.d[4], D.d[5]), add2(D.d[6], D.d[7])));
+                    const f2 v = add2(add2(add2(D.d[0], D.d[1]), add2(D.d[2], D.d[3])),
+                                      add2(add2(D.d[4], D.d[5]), add2(D.d[6], D.d[7])));
+                    ol[j] = lo(v);
+                    oh[j] = hi(v);
                     r = false;
                 }
 #else
-                out[j] = map_pair(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j],
-                                  q[j + 1], q[j + 2], W[j], W[j + 1], hc[j], tm[j], r);
+                map_pair_s(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j], q[j + 1],
+                           q[j + 2], W[j], W[j + 1], hc[j], tm[j], ol[j], oh[j], r);
 #endif
                 rare |= r;
             }
             if (__any_sync(kFull, rare)) {  // rare: near ties / exact opposite-sign ties
                 if (rare) {
 #pragma unroll
-                    for (int j = 0; j < kMapCols; ++j)
-                        out[j] = map_pair_fix(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2],
-                                              q[j], q[j + 1], q[j + 2], out[j]);
+                    for (int j = 0; j < kMapCols; ++j) {
+                        const f2 hw = map_pair_fix(m[j], m[j + 1], m[j + 2], o[j], o[j + 1],
+                                                   o[j + 2], q[j], q[j + 1], q[j + 2],
+                                                   pk(ol[j], oh[j]));
+                        ol[j] = lo(hw);
+                        oh[j] = hi(hw);
+                    }
                 }
             }
             if constexpr (ENERGY) {  // the energy's segment sum of this row
@@ -392,7 +423,7 @@ struct MapWarp {
 #pragma unroll
                     for (int j = 0; j < kMapCols; ++j) {
                         const int xa = x0 + kMapCols * lane + kMapChunk * c + j;
-                        const float hv = c ? hi(out[j]) : lo(out[j]);
+                        const float hv = c ? oh[j] : ol[j];
                         t[kMapCols * c + j] =
                             (INTERIOR || xa < p.w) ? energy_term<QK>(hv, p.q) : 0.0;
                     }
@@ -404,7 +435,7 @@ struct MapWarp {
                         acc;
             }
             if (!ENERGY || p.dst) {
-                store(sp, out);
+                store(sp, ol, oh);
                 sp += dpitch;
             }
         }
@@ -447,6 +478,7 @@ __global__ void __launch_bounds__(32 * kMapWarps, QK ? CF_MAP_MINB_ENERGY : CF_M
         mw.x0 = x0;
         mw.src = src;
         mw.pf_step = p.src_pitch * 4;
+        mw.tail4 = lane < 4;
         mw.yp = ys - 1;
         mw.sbase = sbase;
         // window columns C*i-1 .. C*i+C: 16-byte chunks C*i/2 + k (swizzled)
