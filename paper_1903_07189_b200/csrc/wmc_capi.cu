@@ -247,6 +247,28 @@ int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
         if (cost < best_cost * 0.999) { best_cost = cost; best = ns; }
         if (tasks > slots * 32) break;
     }
+#ifndef CF_MAP_TAIL_MODEL
+#define CF_MAP_TAIL_MODEL 1
+#endif
+    // Images that need several waves: the block scheduler balances many
+    // short tasks better than a few whole waves of long ones, so cost the
+    // work spread over the slots plus one task of tail instead (16384^2:
+    // 55 strips of 298 rows in 2 waves -> ~240 of 69 rows, 0.565 -> 0.547
+    // ms; one-wave images keep the wave count, where it measured better).
+    const int sr_w = (h + best - 1) / best;  // the wave model's choice
+    if (CF_MAP_TAIL_MODEL && cols * ((h + sr_w - 1) / sr_w) > slots) {
+        best_cost = 1e300;
+        for (int ns = 1; ns <= max_strips; ++ns) {
+            const int sr = (h + ns - 1) / ns;
+            const int64_t tasks = cols * ((h + sr - 1) / sr);
+            const double cost = ((double)tasks / (double)slots + 1.0) * (sr + 8.0);
+            if (cost < best_cost * 0.999) { best_cost = cost; best = ns; }
+            if (tasks > slots * 32) break;
+        }
+    }
+#ifdef CF_MAP_FORCE_NS  // experiments: a fixed number of strips
+    best = std::min(CF_MAP_FORCE_NS, h);
+#endif
     p.strip_rows = (h + best - 1) / best;
     p.n_strips = (h + p.strip_rows - 1) / p.strip_rows;
     const int64_t tasks = cols * p.n_strips;
