@@ -186,6 +186,9 @@ constexpr int kMapRowBytes = 8 * (kMapChunk + 2);  // pairs for window columns -
 #endif
 constexpr int kMapWarps = CF_MAP_WARPS;       // warps per block
 static_assert(kMapRing >= kMapPD + 2, "ring too small for the prefetch distance");
+#ifndef CF_MAP_ROLL
+#define CF_MAP_ROLL 0   // 1: rows rolled through registers, loop unrolled x3 (experiment)
+#endif
 
 struct MapParams {
     const float* src;
@@ -333,6 +336,95 @@ struct MapWarp {
         }
     }
 
+    // One output row y: rows y-1, y in m, o (ROLL) or loaded here, y+1 into q.
+    template <bool ROLL>
+    __device__ __forceinline__ void row_step(int y, f2 (&m)[kMapNb], f2 (&o)[kMapNb],
+                                             f2 (&q)[kMapNb], float*& sp, int64_t dpitch) {
+        const int k = y - ys;  // slot of row y-1
+        // rows y-1 .. y+1 landed: of the PD + k groups issued (rows up to
+        // y+PD-2), at most PD-3 may still be pending
+        asm volatile("cp.async.wait_group %0;" ::"n"(kMapPD - 3) : "memory");
+        __syncwarp();
+        if (yp <= ye) prefetch_next(k + kMapPD);  // row y+PD-1 (the strip needs rows <= ye)
+        cp_async_commit();
+        if (!ROLL) {  // rows y-1 and y too (rolled: already in registers)
+            lds_row6(slot(k), co, m);
+            lds_row6(slot(k + 1), co, o);
+        }
+        lds_row6(slot(k + 2), co, q);
+        f2 V[kMapNb], W[kMapNb - 1];
+        float ol[kMapCols], oh[kMapCols];  // chunk 0 / chunk 1 results
+#pragma unroll
+        for (int i = 0; i < kMapNb; ++i) V[i] = add2(m[i], q[i]);
+#pragma unroll
+        for (int i = 0; i < kMapNb - 1; ++i) W[i] = add2(V[i], V[i + 1]);
+        bool rare = false;
+#pragma unroll
+        for (int j = 0; j < kMapCols; ++j) {
+            bool r;
+#if defined(CF_MAP_EXP) && CF_MAP_EXP == 1  // diagnostic (wrong results): data movement only
+            {
+                const f2 v = add2(add2(m[j + 1], q[j + 1]), W[j]);
+                ol[j] = lo(v);
+                oh[j] = hi(v);
+            }
+            r = false;
+#elif defined(CF_MAP_EXP) && CF_MAP_EXP == 2  // diagnostic (wrong results): no selection
+            {
+                PairD D;
+                f2 hb, t0;
+                pair_d(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j], q[j + 1],
+                       q[j + 2], W[j], W[j + 1], hc[j], tm[j], hb, t0, D);
+                hc[j] = hb;
+                tm[j] = t0;
+                const f2 v = add2(add2(add2(D.d[0], D.d[1]), add2(D.d[2], D.d[3])),
+                                  add2(add2(D.d[4], D.d[5]), add2(D.d[6], D.d[7])));
+                ol[j] = lo(v);
+                oh[j] = hi(v);
+                r = false;
+            }
+#else
+            map_pair_s(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j], q[j + 1],
+                       q[j + 2], W[j], W[j + 1], hc[j], tm[j], ol[j], oh[j], r);
+#endif
+            rare |= r;
+        }
+        if (__any_sync(kFull, rare)) {  // rare: near ties / exact opposite-sign ties
+            if (rare) {
+#pragma unroll
+                for (int j = 0; j < kMapCols; ++j) {
+                    const f2 hw = map_pair_fix(m[j], m[j + 1], m[j + 2], o[j], o[j + 1],
+                                               o[j + 2], q[j], q[j + 1], q[j + 2],
+                                               pk(ol[j], oh[j]));
+                    ol[j] = lo(hw);
+                    oh[j] = hi(hw);
+                }
+            }
+        }
+        if constexpr (ENERGY) {  // the energy's segment sum of this row
+            double t[2 * kMapCols];
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int j = 0; j < kMapCols; ++j) {
+                    const int xa = x0 + kMapCols * lane + kMapChunk * c + j;
+                    const float hv = c ? oh[j] : ol[j];
+                    t[kMapCols * c + j] =
+                        (INTERIOR || xa < p.w) ? energy_term<QK>(hv, p.q) : 0.0;
+                }
+            double acc = lane_tree8(t);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, o));
+            if (lane == 0)
+                p.seg_sums[(int64_t)(x0 / (2 * kMapChunk)) * p.planes * p.h + plane_row0 + y] =
+                    acc;
+        }
+        if (!ENERGY || p.dst) {
+            store(sp, ol, oh);
+            sp += dpitch;
+        }
+    }
+
     __device__ __forceinline__ void run(float* dst) {
         // prologue: rows ys-1 .. ys-1+PD-1 -> slots 0 .. PD-1, a group each
 #pragma unroll
@@ -355,90 +447,29 @@ struct MapWarp {
         }
         float* sp = dst ? dst + (int64_t)ys * p.dst_pitch + x0 + kMapCols * lane : nullptr;
         const int64_t dpitch = p.dst_pitch;
-        for (int y = ys; y < ye; ++y) {
-            const int k = y - ys;  // slot of row y-1
-            // rows y-1 .. y+1 landed: of the PD + k groups issued (rows up to
-            // y+PD-2), at most PD-3 may still be pending
-            asm volatile("cp.async.wait_group %0;" ::"n"(kMapPD - 3) : "memory");
-            __syncwarp();
-            if (yp <= ye) prefetch_next(k + kMapPD);  // row y+PD-1 (the strip needs rows <= ye)
-            cp_async_commit();
-            f2 m[kMapNb], o[kMapNb], q[kMapNb];
-            lds_row6(slot(k), co, m);
-            lds_row6(slot(k + 1), co, o);
-            lds_row6(slot(k + 2), co, q);
-            f2 V[kMapNb], W[kMapNb - 1];
-            float ol[kMapCols], oh[kMapCols];  // chunk 0 / chunk 1 results
-#pragma unroll
-            for (int i = 0; i < kMapNb; ++i) V[i] = add2(m[i], q[i]);
-#pragma unroll
-            for (int i = 0; i < kMapNb - 1; ++i) W[i] = add2(V[i], V[i + 1]);
-            bool rare = false;
-#pragma unroll
-            for (int j = 0; j < kMapCols; ++j) {
-                bool r;
-#if defined(CF_MAP_EXP) && CF_MAP_EXP == 1  // diagnostic (wrong results): data movement only
-                {
-                    const f2 v = add2(add2(m[j + 1], q[j + 1]), W[j]);
-                    ol[j] = lo(v);
-                    oh[j] = hi(v);
-                }
-                r = false;
-#elif defined(CF_MAP_EXP) && CF_MAP_EXP == 2  // diagnostic (wrong results): no selection
-                {
-                    PairD D;
-                    f2 hb, t0;
-                    pair_d(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j], q[j + 1],
-                           q[j + 2], W[j], W[j + 1], hc[j], tm[j], hb, t0, D);
-                    hc[j] = hb;
-                    tm[j] = t0;
-                    const f2 v = add2(add2(add2(D.d[0], D.d[1]), add2(D.d[2], D.d[3])),
-                                      add2(add2(D.d[4], D.d[5]), add2(D.d[6], D.d[7])));
-                    ol[j] = lo(v);
-                    oh[j] = hi(v);
-                    r = false;
-                }
-#else
-                map_pair_s(m[j], m[j + 1], m[j + 2], o[j], o[j + 1], o[j + 2], q[j], q[j + 1],
-                           q[j + 2], W[j], W[j + 1], hc[j], tm[j], ol[j], oh[j], r);
-#endif
-                rare |= r;
+#if CF_MAP_ROLL
+        // rows rolled through three register sets: one LDS row per step
+        {
+            f2 ra[kMapNb], rb[kMapNb], rc[kMapNb];
+            lds_row6(slot(0), co, ra);
+            lds_row6(slot(1), co, rb);
+            int y = ys;
+            for (; y + 3 <= ye; y += 3) {
+                row_step<true>(y, ra, rb, rc, sp, dpitch);
+                row_step<true>(y + 1, rb, rc, ra, sp, dpitch);
+                row_step<true>(y + 2, rc, ra, rb, sp, dpitch);
             }
-            if (__any_sync(kFull, rare)) {  // rare: near ties / exact opposite-sign ties
-                if (rare) {
-#pragma unroll
-                    for (int j = 0; j < kMapCols; ++j) {
-                        const f2 hw = map_pair_fix(m[j], m[j + 1], m[j + 2], o[j], o[j + 1],
-                                                   o[j + 2], q[j], q[j + 1], q[j + 2],
-                                                   pk(ol[j], oh[j]));
-                        ol[j] = lo(hw);
-                        oh[j] = hi(hw);
-                    }
-                }
-            }
-            if constexpr (ENERGY) {  // the energy's segment sum of this row
-                double t[2 * kMapCols];
-#pragma unroll
-                for (int c = 0; c < 2; ++c)
-#pragma unroll
-                    for (int j = 0; j < kMapCols; ++j) {
-                        const int xa = x0 + kMapCols * lane + kMapChunk * c + j;
-                        const float hv = c ? oh[j] : ol[j];
-                        t[kMapCols * c + j] =
-                            (INTERIOR || xa < p.w) ? energy_term<QK>(hv, p.q) : 0.0;
-                    }
-                double acc = lane_tree8(t);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, o));
-                if (lane == 0)
-                    p.seg_sums[(int64_t)(x0 / (2 * kMapChunk)) * p.planes * p.h + plane_row0 + y] =
-                        acc;
-            }
-            if (!ENERGY || p.dst) {
-                store(sp, ol, oh);
-                sp += dpitch;
+            for (; y < ye; ++y) {
+                f2 m[kMapNb], o[kMapNb], q[kMapNb];
+                row_step<false>(y, m, o, q, sp, dpitch);
             }
         }
+#else
+        for (int y = ys; y < ye; ++y) {
+            f2 m[kMapNb], o[kMapNb], q[kMapNb];
+            row_step<false>(y, m, o, q, sp, dpitch);
+        }
+#endif
         asm volatile("cp.async.wait_group 0;" ::: "memory");  // no copy outlives the warp
     }
 };
