@@ -261,7 +261,10 @@ int launch_map(const float* in, float* out, int32_t w, int32_t h, int64_t pitch,
         for (int ns = 1; ns <= max_strips; ++ns) {
             const int sr = (h + ns - 1) / ns;
             const int64_t tasks = cols * ((h + sr - 1) / sr);
-            const double cost = ((double)tasks / (double)slots + 1.0) * (sr + 8.0);
+#ifndef CF_MAP_TAIL_OVH
+#define CF_MAP_TAIL_OVH 8.0
+#endif
+            const double cost = ((double)tasks / (double)slots + 1.0) * (sr + CF_MAP_TAIL_OVH);
             if (cost < best_cost * 0.999) { best_cost = cost; best = ns; }
             if (tasks > slots * 32) break;
         }
